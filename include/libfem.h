@@ -1,0 +1,183 @@
+/* libfem.h — C ABI of the B200-native MetaFEM assembly path (arXiv:2111.03541).
+ *
+ * The paper states that the linear system K x = d "is uniquely described by":
+ *   1. PDE weak forms (domain, boundary, stabilization)     -> fem_problem.terms[] (form ids below)
+ *   2. linearization, complete gradient of nonlinear terms   -> fixed device integrands per form
+ *   3. element type and order                                 -> fem_problem.etype / order
+ *   4. quadrature order or scheme                             -> fem_problem.quad_order
+ *   5. temporal discretization scheme                         -> fem_problem.time
+ *   6. the numbering of variables                             -> fixed: κ-major, g(κ,α) = κ·N + α
+ *      (Block B-3: α'(κ,α) = (κ-1)α̂ + α, 0-based here; readings L2/L3 in DESIGN.md)
+ * "which the kernel 'simply' assembles".  The four calls of the hot path are
+ * fem_mesh_create (Block B-1 input), fem_pattern_build (B-1 item 4 + B-4 as CSR + slot map),
+ * fem_assemble_matrix (D-3) and fem_assemble_residual (D-2).
+ *
+ * Conventions
+ *  - 0-based indices.  Arrays are plain pointers; which side (host/device) is stated per argument.
+ *  - Stream arguments are a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Assembly calls are stream-ordered and never synchronize the host.
+ *  - Every function returns 0 on success or a negative FEM_E* code; fem_last_error() returns a
+ *    thread-local message for the last failure.  No C++ exception crosses the ABI; nothing aborts.
+ *  - Device-detected errors (det J <= 0 at a quadrature point) set a per-mesh device error
+ *    word read by fem_get_status (which synchronizes the stream).
+ */
+#ifndef LIBFEM_H
+#define LIBFEM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes */
+#define FEM_OK 0
+#define FEM_E_INVALID_ARG (-1)
+#define FEM_E_UNSUPPORTED (-2)      /* element/order/quadrature/form combination not built      */
+#define FEM_E_INDEX_OVERFLOW (-3)   /* a count exceeds the index width (int32 columns/slots)      */
+#define FEM_E_INVERTED_ELEMENT (-4) /* det J <= 0 at some quadrature point                */
+#define FEM_E_CUDA (-6)
+#define FEM_E_OOM (-8)
+
+/* ---- element types (reading L7: VTK node orders; reference simplex / [-1,1]^3 cube) */
+#define FEM_TRI 1 /* order 1: 3 nodes                                   */
+#define FEM_TET 2 /* order 1: 4 nodes; order 2: 10 nodes (VTK edge order) */
+#define FEM_HEX 4 /* order 1: 8 nodes                                   */
+
+/* ---- physics (κ̂ = number of scalar basic variables, reading L2/L3) */
+#define FEM_THERMAL 1    /* κ̂ = 1: T  */
+#define FEM_ELASTICITY 2 /* κ̂ = dim: d_1..d_dim  */
+#define FEM_NS 3         /* κ̂ = dim+1: u_1..u_dim, p (3D, P1 only)  */
+
+/* ---- weak forms: the paper's named groups; params[] layout per form */
+#define FEM_WF_THERMAL_DOMAIN 0   /* -C(T,T_t) - k(T_,i,T_,i) + (T,s)    P:821,832 params {C, k, s, source_kind(0 const, 1 s·Π sin(π x_d))} */
+#define FEM_WF_THERMAL_CONV_RAD 1 /* h(T,T_env-T) + e_m σ^b(T,T_env^4-T^4) P:822,834 params {h, T_env, e_m, σ^b} */
+#define FEM_WF_THERMAL_FIX 2      /* h_p(T,T_fix-T) + k(T, n_i T_,i)     P:823,835 params {h_p, T_fix, k} */
+#define FEM_WF_ELAST_DOMAIN 3     /* -(ε_ij, σ_ij)                       P:904,920 params {E, ν} */
+#define FEM_WF_ELAST_FIX_ALL 4    /* τ(d_i, d^w_i - d_i)                 P:906,921 params {τ, d^w_1, d^w_2, d^w_3} */
+#define FEM_WF_ELAST_FIX_D1 5     /* τ(d_1, d^w_1 - d_1)                 P:922     params {τ, d^w_1} */
+#define FEM_WF_ELAST_LOAD 6       /* (d_i, σ^l_ij n_j)                   P:905,923 params {σ^l_11..σ^l_33 row-major} */
+#define FEM_WF_NS_DOMAIN 7        /* NS_domain = BASE + SUPG             P:982-983,1003-1008,1022 params {ρ, μ, τ^m, τ^c} */
+#define FEM_WF_NS_BND_INFLOW 8    /* BASE + INFLOW, u^w of P:1050        P:988-990,1009-1013,1023 params {ρ, μ, τ^b, U, H} */
+#define FEM_WF_NS_BND_OUTFLOW 9   /* BASE + OUTFLOW                      P:991,1015,1024 params {ρ, μ} */
+#define FEM_WF_NS_BND_FIX 10      /* BASE + FIX                          P:992,1017-1018,1025 params {ρ, μ, τ^b} */
+
+/* ---- scatter modes ("(atomic) increment") */
+#define FEM_SCATTER_ATOMIC 0   /* element-parallel, fp64 atomicAdd into values/rhs                  */
+#define FEM_SCATTER_COLOURED 1 /* element colours in fixed order, plain RMW: bit-exact run-to-run   */
+#define FEM_SCATTER_TILED 2    /* node-tile owner gather: each row written once, deterministic;
+                                  writes every owned row completely (accumulate must be 0)          */
+
+#define FEM_TIME_STATIC 0
+#define FEM_TIME_GENALPHA 1
+
+typedef struct {
+  int kind;   /* FEM_TIME_STATIC (ν̂ = 0, c1 := 1, reading L12) or FEM_TIME_GENALPHA            */
+  int nu_hat; /* highest time-derivative order carried by the state (0..2)                      */
+  double dt, b1, b2, c1, c2, c3; /* Eq. time_constraints/time_effective               */
+} fem_time_scheme;
+
+#define FEM_MAX_TERMS 16
+#define FEM_MAX_PARAMS 16
+typedef struct {
+  int form;   /* FEM_WF_*                                     */
+  int region; /* -1 = domain Ω, k >= 0 = boundary facet set k */
+  double params[FEM_MAX_PARAMS];
+} fem_term;
+
+typedef struct {
+  int etype, order;
+  int quad_order; /* hex: Gauss-Legendre points per axis (1..3); tri/tet: exactness degree (1..2) */
+  int physics;    /* FEM_THERMAL | FEM_ELASTICITY | FEM_NS                                        */
+  fem_time_scheme time;
+  int n_terms;
+  fem_term terms[FEM_MAX_TERMS];
+} fem_problem;
+
+typedef struct fem_mesh_s* fem_mesh_t;
+typedef struct fem_pattern_s* fem_pattern_t;
+
+/* fem_mesh_create — Block B-1 input: the element→control-point map α(β^el, β^el_cp).
+ *  prob        host; element type/order/physics/quadrature (validated here).
+ *  dim         2 (FEM_TRI) or 3.
+ *  n_nodes     N, number of control points (global numbering).
+ *  coords      HOST, float64 SoA [dim][N].
+ *  n_elems     E; conn HOST int32 SoA [n_loc][E] (VTK local order), values in [0, N).
+ *  bsets       n_bsets boundary facet sets; set k = (bset_elem[k][m], bset_facet[k][m]) HOST arrays of
+ *              length bset_len[k]: element id and local facet (reading L8).
+ *  own_lo/hi   rows assembled by this mesh: control points [own_lo, own_hi) (multi-GPU partition;
+ *              [0, N) on one GPU).  Elements must include every element touching an owned point.
+ *  stream      used for the host→device copies; the call synchronizes it before returning.
+ * The library copies everything into its own device memory (freed by fem_mesh_destroy), builds the
+ * deterministic element colouring and the node-tile schedule.  Errors: INVALID_ARG (sizes/ids out of
+ * range), UNSUPPORTED (combination), OOM, CUDA. */
+int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const double* coords,
+                    int64_t n_elems, const int32_t* conn, int n_bsets, const int64_t* bset_len,
+                    const int32_t* const* bset_elem, const int8_t* const* bset_facet,
+                    int64_t own_lo, int64_t own_hi, void* stream, fem_mesh_t* out);
+
+/* fem_pattern_build — Block B-1 item 4 ("each unique pair is only kept once"), A-3 symbol
+ * pairs (all (κ0,κλ), reading L6) and B-4 realised as a CSR matrix with ascending columns:
+ * row r = κ0·n_own + (α1 - own_lo) holds columns κλ·N + α2 for κλ ascending, α2 ascending.  Also
+ * builds the element→slot map slot_s[(a·n_loc+b)·E + e] = position of (α(e,a), α(e,b)) in the
+ * scalar-graph CSR (rowptr_s over owned points, colidx_s), -1 if α(e,a) is not owned.
+ * Synchronizes `stream` once (to read nnz).  Outputs (host): *n_rows = κ̂·n_own, *nnz.
+ * Errors: INDEX_OVERFLOW (scalar nnz >= 2^31 or κ̂·N >= 2^31), OOM, CUDA. */
+int fem_pattern_build(fem_mesh_t mesh, void* stream, fem_pattern_t* out, int64_t* n_rows,
+                      int64_t* nnz);
+int64_t fem_pattern_nnz_s(fem_pattern_t pat);
+
+/* fem_pattern_export — copy the library-owned pattern into caller DEVICE buffers (any may be NULL):
+ * rowptr int64[n_rows+1], colidx int32[nnz], slot_s int32[n_loc²·E], rowptr_s int64[n_own+1],
+ * colidx_s int32[nnz_s].  Stream-ordered. */
+int fem_pattern_export(fem_pattern_t pat, int64_t* rowptr, int32_t* colidx, int32_t* slot_s,
+                       int64_t* rowptr_s, int32_t* colidx_s, void* stream);
+
+/* fem_assemble_matrix — D-3: values[β^sp] (+)= Σ_γ w_γ f_ν (D0 N̄_a D_λ N_b) ∂L^a/∂λ,
+ * f_ν = c_{ν+1}/Π_{β'≤ν}(b_β' Δt) (Eq. gen_alpha; reading L13).
+ *  state   DEVICE float64 [ν̂+1][κ̂][N]: effective values ∂_t^ν φ̃ (D-1 output).
+ *  values  DEVICE float64 [nnz] (caller-owned).  accumulate = 0: cleared first ("cleared first",
+ *          P:441); 1: added to the existing contents (not allowed with FEM_SCATTER_TILED).
+ *  scatter FEM_SCATTER_*.  prob must match the mesh's element/physics.  No host sync, no allocation. */
+int fem_assemble_matrix(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* prob,
+                        const double* state, double* values, int accumulate, int scatter,
+                        void* stream);
+
+/* fem_assemble_residual — D-2: rhs[g(κ0,α(e,a)) local] (+)= Σ_γ w_γ (D0 N̄_a) L^a(...).
+ *  rhs DEVICE float64 [κ̂·n_own]; other arguments as fem_assemble_matrix.  `pat` may be NULL for the
+ *  atomic and coloured modes (the residual needs no sparsity pattern). */
+int fem_assemble_residual(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* prob,
+                          const double* state, double* rhs, int accumulate, int scatter,
+                          void* stream);
+
+/* fem_assemble_system — D-2 and D-3 in one pass over the elements (one Newton linearisation). */
+int fem_assemble_system(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* prob,
+                        const double* state, double* values, double* rhs, int accumulate,
+                        int scatter, void* stream);
+
+/* fem_residual_norms — norms_dev[0] = Σ_i d_i², norms_dev[1] = max_i |d_i| over the κ̂·n_own owned rows
+ * (the D-2 convergence test).  DEVICE output, stream-ordered. */
+int fem_residual_norms(fem_mesh_t mesh, const double* rhs, double* norms_dev, void* stream);
+
+/* fem_linearize_host — end-to-end call with HOST buffers: copies the state from (pinned) host memory
+ * into library scratch, runs fem_assemble_system into the DEVICE values/rhs, computes the residual
+ * norms and copies them to norms_host[2]; synchronizes the stream before returning. */
+int fem_linearize_host(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* prob,
+                       const double* state_host, double* values, double* rhs, double* norms_host,
+                       int scatter, void* stream);
+
+/* fem_get_status — synchronizes `stream`; returns 0 or FEM_E_INVERTED_ELEMENT (bad_elem = an
+ * offending element id, else -1).  Resets the device error word. */
+int fem_get_status(fem_mesh_t mesh, void* stream, int64_t* bad_elem);
+
+/* fem_mesh_info — host query: n_loc, kappa_hat, number of colours, number of node tiles. */
+int fem_mesh_info(fem_mesh_t mesh, int* n_loc, int* kappa_hat, int* n_colours, int64_t* n_tiles);
+
+void fem_pattern_destroy(fem_pattern_t pat);
+void fem_mesh_destroy(fem_mesh_t mesh);
+const char* fem_last_error(void);
+int fem_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -93,7 +93,7 @@ def lib():
             getattr(L, f).restype = I64
             getattr(L, f).argtypes = [P]
         L.or_get.argtypes = [P] + [P] * 9
-        L.or_get_slot.argtypes = [P, P]
+        L.or_get_slot.argtypes = [P, P, P]
         L.or_free.argtypes = [P]
         L.or_qp_data.argtypes = [C.POINTER(_Problem), I64, P, I64, P, I64, C.c_int, P, P, P, P, P]
         _lib = L
@@ -160,7 +160,7 @@ def assemble(mesh, prob, state, row_mask=None, matrix=True, residual=True, slot=
                                                "rhs", "abs_d", "rowptr_s", "colidx_s")])
         if slot:
             out["slot_s"] = np.empty((mesh.n_loc * mesh.n_loc, mesh.n_elems), np.int32)
-            L.or_get_slot(h, _ptr(out["slot_s"]))
+            L.or_get_slot(h, _ptr(conn), _ptr(out["slot_s"]))
         return out
     finally:
         L.or_free(h)

@@ -551,7 +551,6 @@ struct or_system {
   double* values;
   double* rhs;
   double* absd;
-  int32_t* slot; /* [nloc*nloc][E] */
 };
 
 static int cmp_i64(const void* x, const void* y) {
@@ -607,25 +606,19 @@ static int build_pattern(or_system* s, const ctx* c) {
           s->colidx[pos++] = (int32_t)((int64_t)kl * N + s->colidx_s[t]);
     }
   s->rowptr[s->n_rows] = pos;
-  /* element -> scalar slot map (binary search of α(e,b) in row α(e,a)) */
-  s->slot = (int32_t*)malloc(sizeof(int32_t) * (size_t)nl * nl * (E > 0 ? E : 1));
-  if (!s->slot) return -1;
-  for (int a = 0; a < nl; a++)
-    for (int b = 0; b < nl; b++)
-      for (int64_t e = 0; e < E; e++) {
-        int64_t r = c->conn[(int64_t)a * E + e], col = c->conn[(int64_t)b * E + e];
-        int32_t sl = -1;
-        if (s->loc[r] >= 0) {
-          int64_t lo = s->rowptr_s[s->loc[r]], hi = s->rowptr_s[s->loc[r] + 1] - 1;
-          while (lo <= hi) {
-            int64_t mid = (lo + hi) / 2;
-            if (s->colidx_s[mid] == col) { sl = (int32_t)mid; break; }
-            if (s->colidx_s[mid] < col) lo = mid + 1; else hi = mid - 1;
-          }
-        }
-        s->slot[((int64_t)a * nl + b) * E + e] = sl;
-      }
   return 0;
+}
+
+
+/* position of column `col` in the scalar row of selected node li (binary search), -1 if absent */
+static int64_t find_pos(const or_system* s, int64_t li, int64_t col) {
+  int64_t lo = s->rowptr_s[li], hi = s->rowptr_s[li + 1] - 1;
+  while (lo <= hi) {
+    int64_t mid = (lo + hi) / 2;
+    if (s->colidx_s[mid] == col) return mid;
+    if (s->colidx_s[mid] < col) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
 }
 
 static double time_factor(const or_problem* P, int nu) { /* Eq. gen_alpha, L12/L13 */
@@ -666,7 +659,7 @@ static void add_point(or_system* s, const ctx* c, const or_term* t, int64_t e, c
       for (int a = 0; a < nl; a++) {
         if (li[a] < 0) continue;
         int64_t deg = s->rowptr_s[li[a] + 1] - s->rowptr_s[li[a]];
-        int32_t sl = s->slot[((int64_t)a * nl + b) * c->E + e];
+        int64_t sl = find_pos(s, li[a], node[b]); /* slot of (α(e,a), α(e,b)) */
         for (int k0 = 0; k0 < kh; k0++) {
           int64_t r = (int64_t)k0 * s->n_sel + li[a];
           int64_t idx = s->rowptr[r] + (int64_t)kl * deg + (sl - s->rowptr_s[li[a]]);
@@ -769,14 +762,20 @@ void or_get(const or_system* s, int64_t* sel_nodes, int64_t* rows, int64_t* rowp
   if (colidx_s) memcpy(colidx_s, s->colidx_s, sizeof(int32_t) * (size_t)s->nnz_s);
 }
 
-void or_get_slot(const or_system* s, int32_t* slot_s) {
-  memcpy(slot_s, s->slot, sizeof(int32_t) * (size_t)s->nloc * s->nloc * (size_t)s->E);
+void or_get_slot(const or_system* s, const int32_t* conn, int32_t* slot_s) {
+  int nl = s->nloc;
+  for (int a = 0; a < nl; a++)
+    for (int b = 0; b < nl; b++)
+      for (int64_t e = 0; e < s->E; e++) {
+        int64_t r = conn[(int64_t)a * s->E + e], col = conn[(int64_t)b * s->E + e];
+        slot_s[((int64_t)a * nl + b) * s->E + e] = s->loc[r] >= 0 ? (int32_t)find_pos(s, s->loc[r], col) : -1;
+      }
 }
 
 void or_free(or_system* s) {
   if (!s) return;
   free(s->sel); free(s->loc); free(s->rowptr_s); free(s->colidx_s); free(s->rowptr);
-  free(s->colidx); free(s->values); free(s->rhs); free(s->absd); free(s->slot);
+  free(s->colidx); free(s->values); free(s->rhs); free(s->absd);
   free(s);
 }
 

@@ -53,7 +53,7 @@ int64_t or_nnz_s(const or_system* s);
 void or_get(const or_system* s, int64_t* sel_nodes, int64_t* rows, int64_t* rowptr, int32_t* colidx,
             double* values, double* rhs, double* abs_d, int64_t* rowptr_s, int32_t* colidx_s);
 /* slot_s[(a*n_loc+b)*E + e] = scalar-CSR position of (α(e,a), α(e,b)), -1 if α(e,a) not selected */
-void or_get_slot(const or_system* s, int32_t* slot_s);
+void or_get_slot(const or_system* s, const int32_t* conn, int32_t* slot_s);
 void or_free(or_system* s);
 
 /* Probe: quadrature-point data of element e (facet < 0: volume rule; else facet `facet`).

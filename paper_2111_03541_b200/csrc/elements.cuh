@@ -1,0 +1,183 @@
+// elements.cuh — reference elements, quadrature rules and facet rules for the device path.
+//
+// PAPER.md: "φ^h = Σ_α N_α φ_α", numerical integration Σ_γ w_γ (...) at x_γ,
+// Lagrange simplex/cube elements.  Readings: L7 VTK node orders,
+// L8 facet numbering with outward normals, L9 quadrature (hex: Gauss-Legendre points per axis;
+// simplices: exactness degree).
+//
+// Facet geometry uses Nanson's relation n dA = det(J) J^{-T} m̂ dÂ, with m̂ the outward reference
+// normal of the facet scaled by (reference facet measure / parameter measure).  Since det J > 0 is
+// enforced, the physical normal is outward by construction (no orientation test needed).
+#pragma once
+#include <cstdint>
+
+namespace fem {
+
+enum { ET_TRI = 1, ET_TET = 2, ET_HEX = 4 };
+
+// ---------------------------------------------------------------- 1D Gauss-Legendre on [-1,1]
+__host__ __device__ inline void gauss_legendre(int n, int i, double& x, double& w) {
+  if (n == 1) { x = 0.0; w = 2.0; return; }
+  if (n == 2) { x = (i == 0 ? -1.0 : 1.0) * 0.57735026918962576451; w = 1.0; return; }
+  // n == 3
+  const double r = 0.77459666924148337704;
+  x = (i == 0) ? -r : (i == 1 ? 0.0 : r);
+  w = (i == 1) ? 8.0 / 9.0 : 5.0 / 9.0;
+}
+
+// ---------------------------------------------------------------- element traits
+template <int ET, int ORD> struct Elem;
+
+// P1 triangle: λ = (1-ξ-η, ξ, η)
+template <> struct Elem<ET_TRI, 1> {
+  static constexpr int DIM = 2, NL = 3, NV = 3, NF = 3;
+  __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[2]) {
+    N[0] = 1.0 - xi[0] - xi[1];
+    N[1] = xi[0];
+    N[2] = xi[1];
+    dN[0][0] = -1.0; dN[0][1] = -1.0;
+    dN[1][0] = 1.0;  dN[1][1] = 0.0;
+    dN[2][0] = 0.0;  dN[2][1] = 1.0;
+  }
+  __host__ __device__ static constexpr int vol_nq(int q) { return q <= 1 ? 1 : 3; }
+  __host__ __device__ static void vol_qp(int q, int i, double* xi, double& w) {
+    if (q <= 1) { xi[0] = xi[1] = 1.0 / 3.0; w = 0.5; return; }
+    const double s = 1.0 / 6.0, t = 2.0 / 3.0;
+    xi[0] = (i == 1) ? t : s;
+    xi[1] = (i == 2) ? t : s;
+    w = 1.0 / 6.0;
+  }
+  __host__ __device__ static constexpr int fac_nq(int q) { return (q + 2) / 2; }
+  // edge f joins vertex f and vertex f+1 (mod 3); parameter s in [0,1]
+  __host__ __device__ static void fac_qp(int q, int f, int i, double* xi, double& w, double* mref) {
+    const double V[3][2] = {{0, 0}, {1, 0}, {0, 1}};
+    double x, wg;
+    gauss_legendre(fac_nq(q), i, x, wg);
+    const double s = 0.5 * (1.0 + x);
+    const int p = f, r = (f + 1) % 3;
+    xi[0] = V[p][0] + s * (V[r][0] - V[p][0]);
+    xi[1] = V[p][1] + s * (V[r][1] - V[p][1]);
+    w = 0.5 * wg;
+    // outward reference normal scaled by edge length: rotate the edge vector clockwise
+    mref[0] = V[r][1] - V[p][1];
+    mref[1] = -(V[r][0] - V[p][0]);
+  }
+};
+
+// P1 / P2 tetrahedra: λ = (1-ξ-η-ζ, ξ, η, ζ); P2 edge nodes (0,1),(1,2),(0,2),(0,3),(1,3),(2,3)
+__host__ __device__ inline void tet_bary(const double* xi, double* L) {
+  L[0] = 1.0 - xi[0] - xi[1] - xi[2];
+  L[1] = xi[0];
+  L[2] = xi[1];
+  L[3] = xi[2];
+}
+__host__ __device__ inline double dbary(int k, int j) { return k == 0 ? -1.0 : (k == j + 1 ? 1.0 : 0.0); }
+
+struct TetRules {
+  __host__ __device__ static constexpr int vol_nq(int q) { return q <= 1 ? 1 : 4; }
+  __host__ __device__ static void vol_qp(int q, int i, double* xi, double& w) {
+    if (q <= 1) { xi[0] = xi[1] = xi[2] = 0.25; w = 1.0 / 6.0; return; }
+    const double a = 0.13819660112501051518, b = 0.58541019662496845446;  // (5∓√5)/20, (5+3√5)/20
+    xi[0] = (i == 1) ? b : a;
+    xi[1] = (i == 2) ? b : a;
+    xi[2] = (i == 3) ? b : a;
+    w = 1.0 / 24.0;
+  }
+  __host__ __device__ static constexpr int fac_nq(int q) { return q <= 1 ? 1 : 3; }
+  // face f = the face opposite vertex f; points = barycentric combinations of its three vertices
+  __host__ __device__ static void fac_qp(int q, int f, int i, double* xi, double& w, double* mref) {
+    const double V[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    int v[3], m = 0;
+    for (int k = 0; k < 4; k++)
+      if (k != f) v[m++] = k;
+    double lam[3];
+    if (q <= 1) { lam[0] = lam[1] = lam[2] = 1.0 / 3.0; w = 0.5; }
+    else {
+      for (int k = 0; k < 3; k++) lam[k] = (k == i) ? 2.0 / 3.0 : 1.0 / 6.0;
+      w = 1.0 / 6.0;
+    }
+    for (int d = 0; d < 3; d++) xi[d] = lam[0] * V[v[0]][d] + lam[1] * V[v[1]][d] + lam[2] * V[v[2]][d];
+    // outward normals of the reference tet, scaled by 2·face area
+    if (f == 0) { mref[0] = mref[1] = mref[2] = 1.0; }
+    else { mref[0] = mref[1] = mref[2] = 0.0; mref[f - 1] = -1.0; }
+  }
+};
+
+template <> struct Elem<ET_TET, 1> : TetRules {
+  static constexpr int DIM = 3, NL = 4, NV = 4, NF = 4;
+  __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
+    double L[4];
+    tet_bary(xi, L);
+    for (int k = 0; k < 4; k++) {
+      N[k] = L[k];
+      for (int j = 0; j < 3; j++) dN[k][j] = dbary(k, j);
+    }
+  }
+};
+
+template <> struct Elem<ET_TET, 2> : TetRules {
+  static constexpr int DIM = 3, NL = 10, NV = 4, NF = 4;
+  __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
+    const int EP[6] = {0, 1, 0, 0, 1, 2}, EQ[6] = {1, 2, 2, 3, 3, 3};
+    double L[4];
+    tet_bary(xi, L);
+    for (int k = 0; k < 4; k++) {
+      N[k] = L[k] * (2.0 * L[k] - 1.0);
+      for (int j = 0; j < 3; j++) dN[k][j] = (4.0 * L[k] - 1.0) * dbary(k, j);
+    }
+    for (int e = 0; e < 6; e++) {
+      const int p = EP[e], q = EQ[e];
+      N[4 + e] = 4.0 * L[p] * L[q];
+      for (int j = 0; j < 3; j++) dN[4 + e][j] = 4.0 * (dbary(p, j) * L[q] + L[p] * dbary(q, j));
+    }
+  }
+};
+
+// Q1 hexahedron on [-1,1]^3, VTK order
+__host__ __device__ inline double hex_sign(int a, int d) {
+  // x: - + + - - + + - ; y: - - + + - - + + ; z: - - - - + + + +
+  if (d == 0) return ((a & 3) == 1 || (a & 3) == 2) ? 1.0 : -1.0;
+  if (d == 1) return ((a & 3) >= 2) ? 1.0 : -1.0;
+  return a >= 4 ? 1.0 : -1.0;
+}
+
+template <> struct Elem<ET_HEX, 1> {
+  static constexpr int DIM = 3, NL = 8, NV = 8, NF = 6;
+  __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
+    for (int a = 0; a < 8; a++) {
+      const double fx = 0.5 * (1.0 + hex_sign(a, 0) * xi[0]);
+      const double fy = 0.5 * (1.0 + hex_sign(a, 1) * xi[1]);
+      const double fz = 0.5 * (1.0 + hex_sign(a, 2) * xi[2]);
+      N[a] = fx * fy * fz;
+      dN[a][0] = 0.5 * hex_sign(a, 0) * fy * fz;
+      dN[a][1] = 0.5 * hex_sign(a, 1) * fx * fz;
+      dN[a][2] = 0.5 * hex_sign(a, 2) * fx * fy;
+    }
+  }
+  __host__ __device__ static constexpr int vol_nq(int q) { return q * q * q; }
+  __host__ __device__ static void vol_qp(int q, int i, double* xi, double& w) {
+    double w0, w1, w2;
+    gauss_legendre(q, i % q, xi[0], w0);
+    gauss_legendre(q, (i / q) % q, xi[1], w1);
+    gauss_legendre(q, i / (q * q), xi[2], w2);
+    w = w0 * w1 * w2;
+  }
+  __host__ __device__ static constexpr int fac_nq(int q) { return q * q; }
+  // faces: 0 x-, 1 x+, 2 y-, 3 y+, 4 z-, 5 z+  (reading L8)
+  __host__ __device__ static void fac_qp(int q, int f, int i, double* xi, double& w, double* mref) {
+    const int axis = f >> 1;
+    const double side = (f & 1) ? 1.0 : -1.0;
+    double s, t, ws, wt;
+    gauss_legendre(q, i % q, s, ws);
+    gauss_legendre(q, i / q, t, wt);
+    const int a1 = (axis + 1) % 3, a2 = (axis + 2) % 3;
+    xi[axis] = side;
+    xi[a1] = s;
+    xi[a2] = t;
+    w = ws * wt;
+    mref[0] = mref[1] = mref[2] = 0.0;
+    mref[axis] = side;
+  }
+};
+
+}  // namespace fem

@@ -1,0 +1,96 @@
+"""FemSystem — torch-tensor convenience wrapper over the libfem C ABI (no compute here)."""
+from __future__ import annotations
+
+import torch
+
+from . import fem
+
+
+class FemSystem:
+    """Owns one libfem mesh + pattern and the caller-side device buffers (values, rhs).
+
+    mesh: fem_inputs.Mesh-like (dim, coords, conn, bsets); problem: fem_inputs.Problem-like.
+    own:  (lo, hi) owned control-point range (multi-GPU partition), default all points.
+    """
+
+    def __init__(self, mesh, problem, own=None, device="cuda", build_pattern=True, stream=None):
+        self.problem = problem
+        self.P = fem.make_problem(problem)
+        self.dim = mesh.dim
+        self.N = mesh.coords.shape[1]
+        self.E = mesh.conn.shape[1]
+        self.n_loc = mesh.conn.shape[0]
+        self.own = (0, self.N) if own is None else tuple(own)
+        self.n_own = self.own[1] - self.own[0]
+        self.device = torch.device(device)
+        self.kh = problem.kappa_hat(mesh.dim)
+        self.mesh_h = fem.fem_mesh_create(problem, mesh, own=self.own, stream=stream)
+        self.pat_h = None
+        self.n_rows = self.kh * self.n_own
+        self.nnz = None
+        if build_pattern:
+            self.pat_h, self.n_rows, self.nnz = fem.fem_pattern_build(self.mesh_h, stream=stream)
+            self.nnz_s = fem.fem_pattern_nnz_s(self.pat_h)
+        self.values = None
+        self.rhs = None
+
+    def info(self):
+        return fem.fem_mesh_info(self.mesh_h)
+
+    def alloc(self, matrix=True, residual=True):
+        if matrix and self.values is None:
+            self.values = torch.empty(self.nnz, dtype=torch.float64, device=self.device)
+        if residual and self.rhs is None:
+            self.rhs = torch.empty(self.n_rows, dtype=torch.float64, device=self.device)
+
+    def export_pattern(self, slot=True):
+        dev = self.device
+        out = dict(rowptr=torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev),
+                   colidx=torch.empty(self.nnz, dtype=torch.int32, device=dev),
+                   rowptr_s=torch.empty(self.n_own + 1, dtype=torch.int64, device=dev),
+                   colidx_s=torch.empty(self.nnz_s, dtype=torch.int32, device=dev))
+        if slot:
+            out["slot_s"] = torch.empty((self.n_loc * self.n_loc, self.E), dtype=torch.int32, device=dev)
+        fem.fem_pattern_export(self.pat_h, out["rowptr"], out["colidx"], out.get("slot_s"), out["rowptr_s"],
+                               out["colidx_s"])
+        return out
+
+    def matrix(self, state, scatter="atomic", accumulate=False):
+        self.alloc(True, False)
+        fem.fem_assemble_matrix(self.mesh_h, self.pat_h, self.problem, state, self.values, int(accumulate),
+                                scatter)
+        return self.values
+
+    def residual(self, state, scatter="atomic", accumulate=False):
+        self.alloc(False, True)
+        fem.fem_assemble_residual(self.mesh_h, self.pat_h, self.problem, state, self.rhs, int(accumulate),
+                                  scatter)
+        return self.rhs
+
+    def system(self, state, scatter="atomic", accumulate=False):
+        self.alloc(True, True)
+        fem.fem_assemble_system(self.mesh_h, self.pat_h, self.problem, state, self.values, self.rhs,
+                                int(accumulate), scatter, P=self.P)
+        return self.values, self.rhs
+
+    def norms(self, rhs=None):
+        out = torch.empty(2, dtype=torch.float64, device=self.device)
+        fem.fem_residual_norms(self.mesh_h, self.rhs if rhs is None else rhs, out)
+        return out
+
+    def status(self):
+        return fem.fem_get_status(self.mesh_h)
+
+    def close(self):
+        if getattr(self, "pat_h", None):
+            fem.fem_pattern_destroy(self.pat_h)
+            self.pat_h = None
+        if getattr(self, "mesh_h", None):
+            fem.fem_mesh_destroy(self.mesh_h)
+            self.mesh_h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

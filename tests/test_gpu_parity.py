@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerance (BASELINE.json north_star, reading L20 in DESIGN.md §4):
+  * pattern (rowptr, colidx, rowptr_s, colidx_s) and slot map: bit-exact;
+  * K: max_ij |K_gpu - K_ora| / max_j |K_ora_ij| <= 1e-12 (row-scaled);
+  * d: max_i |d_gpu - d_ora| / max(|d_ora_i|, A_d[i]) <= 1e-12, A_d = Σ|qp contributions|;
+  * coloured / tiled scatter: bit-identical run to run.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from fem_inputs import make_config, make_state  # noqa: E402
+from fem_inputs.configs import TimeScheme  # noqa: E402
+from helpers import csr_row_scaled_err, rhs_err  # noqa: E402
+
+TOL = 1e-12
+
+SMALL = {  # sizes the oracle finishes in seconds; several CTA batches / tiles and a ragged tail
+    "c1": (8,), "c2": (9, 7, 6), "c3": (7, 3, 2), "c4": (9, 4, 3), "c5": (7, 5, 6)}
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _gpu_system(m, p, own=None):
+    from paper_2111_03541_b200 import FemSystem
+    return FemSystem(m, p, own=own)
+
+
+def _to_dev(st):
+    return torch.from_numpy(st).cuda()
+
+
+SCATTERS = os.environ.get("FEM_SCATTERS", "atomic,coloured,tiled").split(",")
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+@pytest.mark.parametrize("variant", ["structured", "perturbed"])
+def test_small_parity_all_modes(name, variant):
+    _need_gpu()
+    m, p = make_config(name, variant, SMALL[name])
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st, slot=True)
+    assert ora["status"] == 0
+    S = _gpu_system(m, p)
+    pat = S.export_pattern()
+    np.testing.assert_array_equal(pat["rowptr"].cpu().numpy(), ora["rowptr"])
+    np.testing.assert_array_equal(pat["colidx"].cpu().numpy(), ora["colidx"])
+    np.testing.assert_array_equal(pat["rowptr_s"].cpu().numpy(), ora["rowptr_s"])
+    np.testing.assert_array_equal(pat["colidx_s"].cpu().numpy(), ora["colidx_s"])
+    np.testing.assert_array_equal(pat["slot_s"].cpu().numpy(), ora["slot_s"])
+    sd = _to_dev(st)
+    for sc in SCATTERS:
+        vals, rhs = S.system(sd, scatter=sc)
+        torch.cuda.synchronize()
+        ek = csr_row_scaled_err(ora["rowptr"], vals.cpu().numpy(), ora["values"])
+        ed = rhs_err(rhs.cpu().numpy(), ora["rhs"], ora["abs_d"])
+        assert ek <= TOL, (sc, ek)
+        assert ed <= TOL, (sc, ed)
+        # matrix-only and residual-only calls agree with the fused call
+        v2 = S.matrix(sd, scatter=sc).clone()
+        r2 = S.residual(sd, scatter=sc).clone()
+        assert csr_row_scaled_err(ora["rowptr"], v2.cpu().numpy(), ora["values"]) <= TOL
+        assert rhs_err(r2.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL
+    assert S.status() == (0, -1)
+    S.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("sc", ["coloured", "tiled"])
+def test_deterministic_modes_bit_exact(name, sc):
+    _need_gpu()
+    m, p = make_config(name, "perturbed", SMALL[name])
+    st = _to_dev(make_state(name, m, p))
+    S = _gpu_system(m, p)
+    ref_v, ref_r = [x.clone() for x in S.system(st, scatter=sc)]
+    for _ in range(3):
+        v, r = S.system(st, scatter=sc)
+        assert torch.equal(v, ref_v) and torch.equal(r, ref_r)
+    S.close()
+
+
+def test_accumulate_and_residual_without_pattern():
+    _need_gpu()
+    from paper_2111_03541_b200 import fem
+    m, p = make_config("c3", "perturbed", SMALL["c3"])
+    st = make_state("c3", m, p)
+    ora = oracle.assemble(m, p, st)
+    S = _gpu_system(m, p)
+    sd = _to_dev(st)
+    v, r = S.system(sd, scatter="atomic")
+    v, r = S.system(sd, scatter="coloured", accumulate=True)
+    assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), 2 * ora["values"]) <= TOL
+    assert rhs_err(r.cpu().numpy(), 2 * ora["rhs"], 2 * ora["abs_d"]) <= TOL
+    rhs = torch.zeros(S.n_rows, dtype=torch.float64, device="cuda")
+    fem.fem_assemble_residual(S.mesh_h, None, p, sd, rhs, 0, "atomic")
+    assert rhs_err(rhs.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL
+    S.close()
+
+
+def test_genalpha_thermal_transient_term():
+    _need_gpu()
+    m, p = make_config("c2", "perturbed", (5, 4, 3))
+    p.time = TimeScheme("genalpha", 1, dt=0.05, b1=0.6, b2=0.5, c1=0.7, c2=0.8, c3=1.0)
+    p.terms[0].params = dict(p.terms[0].params, C=3.0)
+    st = make_state("c2", m, p)
+    ora = oracle.assemble(m, p, st)
+    S = _gpu_system(m, p)
+    for sc in SCATTERS:
+        v, r = S.system(_to_dev(st), scatter=sc)
+        assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL
+        assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL
+    S.close()
+
+
+def test_inverted_element_reported_and_edge_cases():
+    _need_gpu()
+    from helpers import REF_TET, one_element, problem
+    from paper_2111_03541_b200 import FemSystem
+    pr = problem("thermal", "tet", 1, [("THERMAL_DOMAIN", -1, dict(C=0.0, k=1.0, s=1.0))])
+    m = one_element("tet", 1, REF_TET[:, [0, 2, 1, 3]])
+    S = FemSystem(m, pr)
+    S.system(torch.zeros((1, 1, 4), dtype=torch.float64, device="cuda"))
+    rc, bad = S.status()
+    assert rc == -4 and bad == 0
+    assert S.status() == (0, -1)  # the error word is reset after reading
+    S.close()
+    # single element, right orientation: matches the oracle
+    m = one_element("tet", 1, REF_TET)
+    ora = oracle.assemble(m, pr, np.zeros((1, 1, 4)))
+    S = FemSystem(m, pr)
+    v, r = S.system(torch.zeros((1, 1, 4), dtype=torch.float64, device="cuda"), scatter="tiled")
+    assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL
+    S.close()
+
+
+def _partition_rows(m, nparts):
+    """Contiguous owned node ranges + elements touching them (the multi-GPU partition)."""
+    from paper_2111_03541_b200.partition import partition_nodes
+    return partition_nodes(m, nparts)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_partitioned_owned_rows_equal_single(name):
+    """Each part assembles only its owned rows (owner computes, one ghost element layer); the
+    concatenated parts reproduce the single-GPU pattern bit-exactly and values within L20."""
+    _need_gpu()
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config(name, "structured", SMALL[name])
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    full = FemSystem(m, p)
+    fp = full.export_pattern(slot=False)
+    sd = _to_dev(st)
+    parts = _partition_rows(m, 3)
+    kh = p.kappa_hat(m.dim)
+    N = m.n_nodes
+    for sc in SCATTERS:
+        got_v = np.zeros(full.nnz)
+        got_r = np.zeros(full.n_rows)
+        for part in parts:
+            S = FemSystem(part.mesh, p, own=part.own)
+            v, r = S.system(sd, scatter=sc)
+            pp = S.export_pattern(slot=False)
+            lo, hi = part.own
+            rp_full = fp["rowptr"].cpu().numpy()
+            rp = pp["rowptr"].cpu().numpy()
+            ci = pp["colidx"].cpu().numpy()
+            vv = v.cpu().numpy()
+            rr = r.cpu().numpy()
+            n_own = hi - lo
+            for k0 in range(kh):
+                g0, g1 = k0 * N + lo, k0 * N + hi
+                a, b = rp_full[g0], rp_full[g1]
+                la, lb = rp[k0 * n_own], rp[(k0 + 1) * n_own]
+                np.testing.assert_array_equal(ci[la:lb], fp["colidx"][a:b].cpu().numpy())
+                got_v[a:b] = vv[la:lb]
+                got_r[g0:g1] = rr[k0 * n_own:(k0 + 1) * n_own]
+            S.close()
+        assert csr_row_scaled_err(ora["rowptr"], got_v, ora["values"]) <= TOL
+        assert rhs_err(got_r, ora["rhs"], ora["abs_d"]) <= TOL
+    full.close()
+
+
+FULL_SAMPLES = 160
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_full_size_sampled_rows(name):
+    """BASELINE.json full sizes, in the launch configuration bench.py times (fused system call):
+    the oracle computes a random sample of rows (plus boundary-touching rows) one by one."""
+    _need_gpu()
+    m, p = make_config(name, "structured")
+    st = make_state(name, m, p)
+    rng = np.random.default_rng(7)
+    sel = np.zeros(m.n_nodes, dtype=bool)
+    sel[rng.choice(m.n_nodes, FULL_SAMPLES, replace=False)] = True
+    for be, _bf in m.bsets:  # rows touched by boundary terms
+        ids = np.unique(m.conn[:, be[rng.choice(len(be), min(8, len(be)), replace=False)]])
+        sel[ids[:24]] = True
+    sel[[0, m.n_nodes - 1]] = True
+    ora = oracle.assemble(m, p, st, row_mask=sel)
+    assert ora["status"] == 0
+    from paper_2111_03541_b200 import FemSystem
+    S = FemSystem(m, p)
+    pat = S.export_pattern(slot=False)
+    rowptr = pat["rowptr"]
+    rows = torch.from_numpy(ora["rows"]).cuda()
+    starts, ends = rowptr[rows], rowptr[rows + 1]
+    lens = (ends - starts).cpu().numpy()
+    np.testing.assert_array_equal(lens, np.diff(ora["rowptr"]))
+    idx = torch.cat([torch.arange(int(a), int(b), device="cuda") for a, b in zip(starts.tolist(), ends.tolist())])
+    np.testing.assert_array_equal(pat["colidx"][idx].cpu().numpy(), ora["colidx"])
+    del pat
+    sd = _to_dev(st)
+    for sc in ["tiled", "atomic"]:
+        v, r = S.system(sd, scatter=sc)
+        assert csr_row_scaled_err(ora["rowptr"], v[idx].cpu().numpy(), ora["values"]) <= TOL, sc
+        assert rhs_err(r[rows].cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL, sc
+    S.close()
