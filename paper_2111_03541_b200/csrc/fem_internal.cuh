@@ -32,18 +32,28 @@ struct TaskList {
   std::vector<int64_t> col_off;  // host, size n_colours+1
 };
 
-// Node-tile schedule (FEM_SCATTER_TILED): owned points split into tiles; for tile t the elements
-// touching it are tile_elem[tile_eoff[t] .. tile_eoff[t+1]).
+// Visits of one tile schedule: for tile t, runs [roff[t], roff[t+1]); run r covers visits
+// [run[r], run[r+1]) which all have the same colour (no two share a control point).
+struct VisitList {
+  int64_t n_runs = 0, n_visits = 0, max_per_tile = 0;
+  int64_t* roff = nullptr;   // device [n_tiles+1]
+  int64_t* run = nullptr;    // device [n_runs+1]
+  int32_t* elem = nullptr;   // device [n_visits]
+  int8_t* facet = nullptr;   // device [n_visits] (boundary sets only)
+};
+
+// Node-tile schedule (FEM_SCATTER_TILED): owned points split into spatially compact tiles whose
+// rows fit the shared-memory accumulator; each tile visits every element touching it.
 struct TileSchedule {
   int64_t n_tiles = 0;
   int max_tile_nodes = 0;
+  int64_t acc_max = 0;           // largest accumulator (doubles) of any tile
   int64_t* tile_noff = nullptr;  // device [n_tiles+1] offsets into tile_node
   int32_t* tile_node = nullptr;  // device: owned points of each tile (ascending)
-  int64_t* tile_eoff = nullptr;  // device [n_tiles+1]
-  int32_t* tile_elem = nullptr;  // device: elements touching each tile
-  int64_t* tile_foff = nullptr;  // device [n_bsets][n_tiles+1] facet offsets per set
-  int32_t* tile_fent = nullptr;  // device: facet-entry indices (into the set's arrays) per tile
-  int64_t max_tile_elems = 0;
+  VisitList dom;                 // element visits
+  std::vector<VisitList> bnd;    // facet visits per boundary set
+  uint8_t* loc = nullptr;        // device [E][n_loc][n_loc]: slot - rowptr_s[α(e,a)] (255: not owned)
+  int64_t visits_total = 0;
 };
 
 }  // namespace fem
@@ -58,15 +68,23 @@ struct fem_mesh_s {
   std::vector<int64_t> bset_len;
   std::vector<int32_t*> bset_elem_dev;  // original order (device)
   std::vector<int8_t*> bset_facet_dev;
-  fem::TileSchedule tiles;
+  // host copies kept for the tile schedule (built at pattern time, needs row degrees)
+  std::vector<int32_t> h_conn;
+  std::vector<double> h_coords;
+  std::vector<uint8_t> h_colour;
+  std::vector<std::vector<int32_t>> h_bset_elem;
+  std::vector<std::vector<int8_t>> h_bset_facet;
+  std::vector<std::vector<uint8_t>> h_bset_colour;
   long long* err = nullptr;     // device error word: an offending element id or -1
   double* scratch_state = nullptr;  // e2e staging buffer (lazily allocated)
   size_t scratch_state_bytes = 0;
   int n_colours = 0;
+  int64_t last_n_tiles = 0;
 };
 
 struct fem_pattern_s {
   fem_mesh_s* mesh = nullptr;
+  fem::TileSchedule tiles;
   int64_t n_rows = 0, nnz = 0, nnz_s = 0;
   int64_t* rowptr_s = nullptr;  // device [n_own+1]
   int32_t* colidx_s = nullptr;  // device [nnz_s]
@@ -97,6 +115,8 @@ int launch_generic(const AsmArgs& A, bool facet);
 int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_problem* prob,
                  const double* state, double* values, double* rhs, cudaStream_t stream);
 int pattern_build(fem_mesh_s* m, cudaStream_t stream, fem_pattern_s* p);
+int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t stream);
+void tiles_free(TileSchedule& T);
 int residual_norms(const fem_mesh_s* m, const double* rhs, double* norms, cudaStream_t stream);
 FormArgs make_form_args(const fem_problem* prob, const fem_term& t);
 

@@ -46,6 +46,12 @@ FormArgs make_form_args(const fem_problem* prob, const fem_term& t) {
   F.f0 = ga ? prob->time.c1 : 1.0;
   F.f1 = ga ? prob->time.c2 / (prob->time.b1 * prob->time.dt) : 0.0;
   for (int i = 0; i < FEM_MAX_PARAMS; i++) F.p[i] = t.params[i];
+  F.lam = F.mu = 0.0;
+  if (t.form == FEM_WF_ELAST_DOMAIN) {
+    const double E = t.params[0], nu = t.params[1];
+    F.lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    F.mu = E / (2.0 * (1.0 + nu));
+  }
   return F;
 }
 
@@ -101,14 +107,8 @@ void fem_mesh_destroy(fem_mesh_t m) {
   for (auto p : m->bset_facet_dev) cudaFree(p);
   cudaFree(m->err);
   if (m->scratch_state) cudaFree(m->scratch_state);
-  TileSchedule& T = m->tiles;
-  cudaFree(T.tile_noff); cudaFree(T.tile_node); cudaFree(T.tile_eoff); cudaFree(T.tile_elem);
-  cudaFree(T.tile_foff); cudaFree(T.tile_fent);
   delete m;
 }
-
-int fem_tiles_build(fem_mesh_s* m, const int32_t* conn, int n_bsets, const int64_t* bset_len,
-                    const int32_t* const* bset_elem, cudaStream_t s);
 
 int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const double* coords, int64_t n_elems,
                     const int32_t* conn, int n_bsets, const int64_t* bset_len, const int32_t* const* bset_elem,
@@ -174,6 +174,11 @@ int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const dou
                            order, m->dom.col_off);
     if (nc < 0) { set_error("fem_mesh_create: colouring needs more than 64 colours"); return fail(FEM_E_UNSUPPORTED); }
     m->n_colours = nc;
+    m->h_colour.resize(n_elems);
+    for (int c = 0; c < nc; c++)
+      for (int64_t j = m->dom.col_off[c]; j < m->dom.col_off[c + 1]; j++) m->h_colour[order[j]] = (uint8_t)c;
+    m->h_conn.assign(conn, conn + (int64_t)nl * n_elems);
+    m->h_coords.assign(coords, coords + (int64_t)dim * n_nodes);
     m->dom.n = n_elems;
     MTRY(cudaMalloc(&m->dom.elem, sizeof(int32_t) * (n_elems > 0 ? n_elems : 1)));
     if (n_elems > 0) MTRY(cudaMemcpyAsync(m->dom.elem, order.data(), sizeof(int32_t) * n_elems, cudaMemcpyHostToDevice, s));
@@ -199,6 +204,11 @@ int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const dou
     int nc = greedy_colour(L, n_nodes, nl, [&](int64_t j, int a) { return conn[(int64_t)a * n_elems + bset_elem[k][j]]; },
                            order, T.col_off);
     if (nc < 0) { set_error("fem_mesh_create: facet colouring needs more than 64 colours"); return fail(FEM_E_UNSUPPORTED); }
+    m->h_bset_elem.emplace_back(bset_elem[k], bset_elem[k] + L);
+    m->h_bset_facet.emplace_back(bset_facet[k], bset_facet[k] + L);
+    m->h_bset_colour.emplace_back(L);
+    for (int c = 0; c + 1 < (int)T.col_off.size(); c++)
+      for (int64_t j = T.col_off[c]; j < T.col_off[c + 1]; j++) m->h_bset_colour[k][order[j]] = (uint8_t)c;
     std::vector<int32_t> te(L);
     std::vector<int8_t> tf(L);
     for (int64_t j = 0; j < L; j++) { te[j] = bset_elem[k][order[j]]; tf[j] = bset_facet[k][order[j]]; }
@@ -211,10 +221,6 @@ int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const dou
     }
     MTRY(cudaStreamSynchronize(s));
   }
-  {
-    int rc = fem_tiles_build(m, conn, n_bsets, bset_len, bset_elem, s);
-    if (rc != 0) return fail(rc);
-  }
   MTRY(cudaStreamSynchronize(s));
 #undef MTRY
   *out = m;
@@ -226,12 +232,13 @@ int fem_mesh_info(fem_mesh_t m, int* n_loc, int* kappa_hat, int* n_colours, int6
   if (n_loc) *n_loc = m->n_loc;
   if (kappa_hat) *kappa_hat = m->kh;
   if (n_colours) *n_colours = m->n_colours;
-  if (n_tiles) *n_tiles = m->tiles.n_tiles;
+  if (n_tiles) *n_tiles = m->last_n_tiles;
   return 0;
 }
 
 void fem_pattern_destroy(fem_pattern_t p) {
   if (!p) return;
+  tiles_free(p->tiles);
   cudaFree(p->rowptr_s); cudaFree(p->colidx_s); cudaFree(p->slot); cudaFree(p->rowptr); cudaFree(p->colidx);
   delete p;
 }
@@ -242,7 +249,9 @@ int fem_pattern_build(fem_mesh_t m, void* stream, fem_pattern_t* out, int64_t* n
   fem_pattern_s* p = new fem_pattern_s();
   p->mesh = m;
   int rc = pattern_build(m, (cudaStream_t)stream, p);
+  if (rc == 0) rc = tiles_build(m, p, (cudaStream_t)stream);
   if (rc != 0) { fem_pattern_destroy(p); return rc; }
+  m->last_n_tiles = p->tiles.n_tiles;
   if (n_rows) *n_rows = p->n_rows;
   if (nnz) *nnz = p->nnz;
   *out = p;

@@ -27,7 +27,8 @@ struct QP {
 struct FormArgs {
   int form;
   int nu_hat;
-  double f0, f1;  // time factors f_0 = c1 (static 1), f_1 = c2/(b1 Δt)
+  double f0, f1;   // time factors f_0 = c1 (static 1), f_1 = c2/(b1 Δt)
+  double lam, mu;  // elasticity: λ = Eν/((1+ν)(1-2ν)), μ = E/(2(1+ν)), precomputed per call
   double p[FEM_MAX_PARAMS];
 };
 
@@ -64,8 +65,7 @@ __device__ __forceinline__ double form_res(const FormArgs& F, const QP<DIM, NL, 
     }
     case FEM_WF_ELAST_DOMAIN: {
       if (KH != DIM) return 0.0;
-      const double E = p[0], nu = p[1];
-      const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
+      const double lam = F.lam, mu = F.mu;
       double div = 0.0;
 #pragma unroll
       for (int d = 0; d < DIM; d++) div += q.gu[d][d];
@@ -177,8 +177,7 @@ __device__ __forceinline__ double form_tan(const FormArgs& F, const QP<DIM, NL, 
       return Na * (p[2] * Gbn - p[0] * Nb) * F.f0;
     }
     case FEM_WF_ELAST_DOMAIN: {
-      const double E = p[0], nu = p[1];
-      const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
+      const double lam = F.lam, mu = F.mu;
       const int i = k0 % DIM, m = kl % DIM;
       double v = lam * q.G[a][i] * q.G[b][m] + mu * q.G[a][m] * q.G[b][i];
       if (i == m) v += mu * GaGb;
