@@ -30,17 +30,17 @@ namespace fem {
 
 constexpr int TILE_MAX_NODES = 512;
 constexpr int64_t ACC_BUDGET_MAX = 16384;  // doubles (128 KB): hard cap of the row accumulator
-static int64_t acc_budget() {  // default 8192 doubles (64 KB) lets two CTAs share an SM
+static int64_t acc_budget() {  // default 16384 doubles (128 KB): one 16-warp CTA per SM
   static int64_t v = [] {
     const char* s = getenv("FEM_TILE_ACC");
-    int64_t x = s ? atoll(s) : 8192;
+    int64_t x = s ? atoll(s) : 16384;
     return x < 256 ? 256 : (x > ACC_BUDGET_MAX ? ACC_BUDGET_MAX : x);
   }();
   return v;
 }
 constexpr int MAX_DOM_TERMS = 4;
 constexpr int MAX_FAC_TERMS = 8;
-constexpr int TILED_THREADS = 256;
+constexpr int TILED_THREADS = 512;
 
 // ------------------------------------------------------------------ host: tile schedule
 static uint64_t spread_bits3(uint64_t x) {  // 21 bits -> every third bit
@@ -307,12 +307,11 @@ struct TiledParams {
   double* rhs;
   long long* err;
   int nu_hat;
-  int vmax;          // capacity of the per-tile visit arrays
-  int bg_dom, bg_fac;  // elements per geometry batch (domain, facets)
-  int qp_bytes;      // bytes of the point-record region
+  int vmax;      // capacity of the per-tile visit arrays
+  int rec_bytes; // bytes of one warp's point-record slot
 };
 
-// Lean point record for elasticity-only domain batches: w, ∇N_a, and w·σ.
+// Lean point record for elasticity-only domain visits: w, ∇N_a, and w·σ.
 template <int DIM, int NL>
 struct QPE {
   double w;
@@ -328,6 +327,14 @@ struct TileCfg {
   using QPG = QPX<DIM, NL, KH>;
   using QPL = QPE<DIM, NL>;
   static constexpr size_t HEAD_BYTES = 20 * TILE_MAX_NODES + 16;
+  static constexpr int WARPS = TILED_THREADS / 32;
+};
+
+// lanes per quadrature point in the cooperative geometry: largest power of two with NQ*NSUB <= 32
+template <int NQ>
+struct Sub {
+  static constexpr int v = NQ >= 32 ? 1 : (NQ * 32 <= 32 ? 32 : (NQ * 16 <= 32 ? 16 : (NQ * 8 <= 32 ? 8 :
+                           (NQ * 4 <= 32 ? 4 : (NQ * 2 <= 32 ? 2 : 1)))));
 };
 
 __device__ __forceinline__ int find_local(const int32_t* __restrict__ tnode, int T, int node) {
@@ -342,52 +349,73 @@ __device__ __forceinline__ int find_local(const int32_t* __restrict__ tnode, int
   return -1;
 }
 
-struct TileSmem {  // per-tile arrays (shared memory)
+template <int NSUB>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = 1; o < NSUB; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct TileSmem {
   int32_t* tnode; int64_t* trps; int32_t* tdeg; int32_t* toff;
+  int32_t* vid;    // [vmax] element id of each visit
+  int8_t* vfac;    // [vmax] facet id
   int32_t* vnode;  // [vmax*NL]
   int16_t* vown;   // [vmax*NL] tile-local point index or -1
-  int16_t* items;  // [vmax*NL] owned (visit, a) pairs, visit-major
-  int32_t* ioff;   // [vmax+1] first item of each visit
-  int32_t* vid;    // [vmax] element id
-  int8_t* vfac;    // [vmax] facet id
-  int8_t* vbad;    // [vmax]
-  unsigned char* qp;  // point records
+  unsigned char* qp;  // per-warp point-record slots
   double* acc;
   double* racc;
   int T;
 };
 
-// Geometry of one quadrature point (A5) + operand fields (A6) of visit v; returns det J.
-template <class EL, int KH, bool FACET>
-__device__ __forceinline__ double point_geometry(const TiledParams& P, const int32_t* __restrict__ nd, int facet, int g,
-                                                 double (&N)[EL::NL], double (&G)[EL::NL][EL::DIM], double& w,
-                                                 double (&x)[EL::DIM], double (&nrm)[EL::DIM], int Q) {
-  constexpr int DIM = EL::DIM, NL = EL::NL;
+// One warp assembles one element (or facet) visit into the tile accumulator.
+template <int ET, int ORD, int KH, int Q, bool FACET, bool LEAN>
+__device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs* forms, int nforms, const TileSmem& S,
+                                           int v, unsigned char* slot) {
+  using C = TileCfg<ET, ORD, KH, Q>;
+  using EL = typename C::EL;
+  constexpr int DIM = C::DIM, NL = C::NL;
+  constexpr int NQ = FACET ? C::NQF : C::NQV;
+  constexpr int NSUB = Sub<NQ>::v;
+  using QPG = typename C::QPG;
+  using QPL = typename C::QPL;
+  const int lane = threadIdx.x & 31;
+  const int32_t* nd = S.vnode + v * NL;
+  const int16_t* own = S.vown + v * NL;
+  // ---- cooperative geometry: lane -> (point g, node group sub)
+  const int g = lane / NSUB, sub = lane % NSUB;
+  const bool gl = g < NQ;
+  const int gq = gl ? g : 0;
   double xi[3] = {0, 0, 0}, wref, mref[3] = {0, 0, 0};
-  if constexpr (FACET) EL::fac_qp(Q, facet, g, xi, wref, mref);
-  else EL::vol_qp(Q, g, xi, wref);
-  double dN[NL][DIM];
+  if constexpr (FACET) EL::fac_qp(Q, S.vfac[v], gq, xi, wref, mref);
+  else EL::vol_qp(Q, gq, xi, wref);
+  double N[NL], dN[NL][DIM];
   EL::shape(xi, N, dN);
-  double J[DIM][DIM];
+  double J[DIM][DIM], xp[DIM];
 #pragma unroll
-  for (int i = 0; i < DIM; i++)
+  for (int i = 0; i < DIM; i++) {
+    xp[i] = 0.0;
 #pragma unroll
     for (int j = 0; j < DIM; j++) J[i][j] = 0.0;
+  }
 #pragma unroll
-  for (int a = 0; a < NL; a++) {
-    double X[DIM];
+  for (int a = 0; a < NL; a++)
+    if (a % NSUB == sub) {
+      double X[DIM];
 #pragma unroll
-    for (int d = 0; d < DIM; d++) X[d] = __ldg(P.coords + (int64_t)d * P.N + nd[a]);
+      for (int d = 0; d < DIM; d++) X[d] = __ldg(P.coords + (int64_t)d * P.N + nd[a]);
 #pragma unroll
-    for (int i = 0; i < DIM; i++)
+      for (int i = 0; i < DIM; i++) {
+        xp[i] = fma(N[a], X[i], xp[i]);
 #pragma unroll
-      for (int j = 0; j < DIM; j++) J[i][j] = fma(X[i], dN[a][j], J[i][j]);
-    if (a == 0) {
-#pragma unroll
-      for (int d = 0; d < DIM; d++) x[d] = 0.0;
+        for (int j = 0; j < DIM; j++) J[i][j] = fma(X[i], dN[a][j], J[i][j]);
+      }
     }
 #pragma unroll
-    for (int d = 0; d < DIM; d++) x[d] = fma(N[a], X[d], x[d]);
+  for (int i = 0; i < DIM; i++) {
+    xp[i] = group_sum<NSUB>(xp[i]);
+#pragma unroll
+    for (int j = 0; j < DIM; j++) J[i][j] = group_sum<NSUB>(J[i][j]);
   }
   double Ji[DIM][DIM], det;
   if constexpr (DIM == 2) {
@@ -409,15 +437,12 @@ __device__ __forceinline__ double point_geometry(const TiledParams& P, const int
     Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
     Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
   }
-#pragma unroll
-  for (int a = 0; a < NL; a++)
-#pragma unroll
-    for (int i = 0; i < DIM; i++) {
-      double sacc = 0.0;
-#pragma unroll
-      for (int j = 0; j < DIM; j++) sacc = fma(Ji[j][i], dN[a][j], sacc);
-      G[a][i] = sacc;
-    }
+  const bool bad = __any_sync(0xffffffffu, gl && !(det > 0.0));
+  if (bad) {
+    if (lane == 0) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)S.vid[v]);
+    return;
+  }
+  double w, nrm[DIM];
   if constexpr (FACET) {  // Nanson: n dA = det(J) J^{-T} m̂ dÂ
     double nn = 0.0;
 #pragma unroll
@@ -437,254 +462,214 @@ __device__ __forceinline__ double point_geometry(const TiledParams& P, const int
     for (int i = 0; i < DIM; i++) nrm[i] = 0.0;
     w = wref * det;
   }
-  return det;
+  // gradients of this lane's nodes and partial operand fields
+  double u0[KH], u1[KH], gu[KH][DIM];
+#pragma unroll
+  for (int k = 0; k < KH; k++) {
+    u0[k] = 0.0;
+    u1[k] = 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; d++) gu[k][d] = 0.0;
+  }
+  QPL* ql = reinterpret_cast<QPL*>(slot);
+  QPG* qg = reinterpret_cast<QPG*>(slot);
+#pragma unroll
+  for (int a = 0; a < NL; a++)
+    if (a % NSUB == sub) {
+      double Ga[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; i++) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; j++) sacc = fma(Ji[j][i], dN[a][j], sacc);
+        Ga[i] = sacc;
+      }
+      if (gl) {
+        if constexpr (LEAN) {
+#pragma unroll
+          for (int i = 0; i < DIM; i++) ql[gq].G[a][i] = Ga[i];
+        } else {
+          qg[gq].N[a] = N[a];
+#pragma unroll
+          for (int i = 0; i < DIM; i++) qg[gq].G[a][i] = Ga[i];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KH; k++) {
+        const double s0 = __ldg(P.state + (int64_t)k * P.N + nd[a]);
+        u0[k] = fma(N[a], s0, u0[k]);
+        if (!LEAN && P.nu_hat >= 1) u1[k] = fma(N[a], __ldg(P.state + ((int64_t)KH + k) * P.N + nd[a]), u1[k]);
+#pragma unroll
+        for (int d = 0; d < DIM; d++) gu[k][d] = fma(Ga[d], s0, gu[k][d]);
+      }
+    }
+#pragma unroll
+  for (int k = 0; k < KH; k++) {
+    u0[k] = group_sum<NSUB>(u0[k]);
+    if (!LEAN) u1[k] = group_sum<NSUB>(u1[k]);
+#pragma unroll
+    for (int d = 0; d < DIM; d++) gu[k][d] = group_sum<NSUB>(gu[k][d]);
+  }
+  if (gl && sub == 0) {
+    if constexpr (LEAN) {
+      ql[gq].w = w;
+      double div = 0.0;
+#pragma unroll
+      for (int k = 0; k < DIM; k++) div += gu[k % KH][k];
+      const double lw = forms[0].lam * w * div, mw = forms[0].mu * w;
+#pragma unroll
+      for (int i = 0; i < DIM; i++)
+#pragma unroll
+        for (int j = 0; j < DIM; j++) ql[gq].S[i][j] = (i == j ? lw : 0.0) + mw * (gu[i % KH][j] + gu[j % KH][i]);
+    } else {
+      QPG& q = qg[gq];
+      q.w = w;
+#pragma unroll
+      for (int d = 0; d < DIM; d++) { q.x[d] = xp[d]; q.n[d] = nrm[d]; }
+#pragma unroll
+      for (int k = 0; k < KH; k++) {
+        q.u[0][k] = u0[k];
+        q.u[1][k] = u1[k];
+#pragma unroll
+        for (int d = 0; d < DIM; d++) q.gu[k][d] = gu[k][d];
+      }
+      if constexpr (KH == DIM + 1) {  // NS strong residuals at the point
+        const double rho = forms[0].p[0];
+        double rc = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; k++) rc += gu[k][k];
+        q.ext[DIM] = rc;
+#pragma unroll
+        for (int i = 0; i < DIM; i++) {
+          double rm = gu[DIM][i];
+#pragma unroll
+          for (int k = 0; k < DIM; k++) rm = fma(rho * u0[k], gu[i][k], rm);
+          q.ext[i] = rm;
+        }
+      }
+      if constexpr (KH == DIM) {
+        if (!FACET && forms[0].form == FEM_WF_ELAST_DOMAIN) {
+          double div = 0.0;
+#pragma unroll
+          for (int k = 0; k < DIM; k++) div += gu[k][k];
+          const double lw = forms[0].lam * w * div, mw = forms[0].mu * w;
+#pragma unroll
+          for (int i = 0; i < DIM; i++)
+#pragma unroll
+            for (int j = 0; j < DIM; j++) q.ext[i * DIM + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // ---- owned test nodes of this visit
+  int owned_a[NL], n_owned = 0;
+#pragma unroll
+  for (int a = 0; a < NL; a++)
+    if (own[a] >= 0) owned_a[n_owned++] = a;
+  const int npair = P.values ? n_owned * NL : 0;
+  const int nres = P.rhs ? n_owned : 0;
+  const int e = S.vid[v];
+  for (int t = lane; t < npair + nres; t += 32) {
+    const bool is_mat = t < npair;
+    const int ia = is_mat ? t / NL : t - npair;
+    int a = 0;
+#pragma unroll
+    for (int k = 0; k < NL; k++)
+      if (k == ia) a = owned_a[k];
+    const int li = own[a];
+    if (is_mat) {
+      const int b = t % NL;
+      const int pos = __ldg(P.loc + (int64_t)e * (NL * NL) + a * NL + b);
+      double K[KH][KH];
+#pragma unroll
+      for (int i = 0; i < KH; i++)
+#pragma unroll
+        for (int m = 0; m < KH; m++) K[i][m] = 0.0;
+      if constexpr (LEAN) {
+        double M[DIM][DIM];
+#pragma unroll
+        for (int j = 0; j < DIM; j++)
+#pragma unroll
+          for (int k = 0; k < DIM; k++) M[j][k] = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < NQ; gg++) {
+          double wa[DIM], gb[DIM];
+          const double wq = ql[gg].w;
+#pragma unroll
+          for (int j = 0; j < DIM; j++) { wa[j] = wq * ql[gg].G[a][j]; gb[j] = ql[gg].G[b][j]; }
+#pragma unroll
+          for (int j = 0; j < DIM; j++)
+#pragma unroll
+            for (int k = 0; k < DIM; k++) M[j][k] = fma(wa[j], gb[k], M[j][k]);
+        }
+        for (int f = 0; f < nforms; f++) {  // every LEAN form is ELAST_DOMAIN
+          const double lam = forms[f].lam, mu = forms[f].mu, f0 = forms[f].f0;
+          double tr = 0.0;
+#pragma unroll
+          for (int j = 0; j < DIM; j++) tr += M[j][j];
+#pragma unroll
+          for (int i = 0; i < DIM; i++)
+#pragma unroll
+            for (int m = 0; m < DIM; m++)
+              K[i % KH][m % KH] -= f0 * (lam * M[i][m] + mu * M[m][i] + (i == m ? mu * tr : 0.0));
+        }
+      } else {
+        for (int f = 0; f < nforms; f++)
+          if (forms[f].form != FEM_WF_ELAST_LOAD) pair_block<DIM, NL, KH, NQ>(forms[f], qg, a, b, K);
+      }
+      const int d = S.tdeg[li];
+      double* rowb = S.acc + S.toff[li] + pos;
+#pragma unroll
+      for (int i = 0; i < KH; i++)
+#pragma unroll
+        for (int m = 0; m < KH; m++) atomicAdd(rowb + (i * KH + m) * d, K[i][m]);
+    } else {
+      double rr[KH];
+#pragma unroll
+      for (int i = 0; i < KH; i++) rr[i] = 0.0;
+      if constexpr (LEAN) {
+#pragma unroll
+        for (int gg = 0; gg < NQ; gg++)
+#pragma unroll
+          for (int i = 0; i < DIM; i++) {
+            double tt = 0.0;
+#pragma unroll
+            for (int j = 0; j < DIM; j++) tt = fma(ql[gg].S[i][j], ql[gg].G[a][j], tt);
+            rr[i % KH] -= tt;
+          }
+      } else {
+        for (int f = 0; f < nforms; f++) row_res<DIM, NL, KH, NQ>(forms[f], qg, a, rr, !FACET && f == 0);
+      }
+#pragma unroll
+      for (int i = 0; i < KH; i++) atomicAdd(S.racc + i * S.T + li, rr[i]);
+    }
+  }
+  __syncwarp();
 }
 
-template <int ET, int ORD, int KH, int Q, bool FACET, bool LEAN>
-__device__ void tile_visits(const TiledParams& P, const VisitList& V, const FormArgs* forms, int nforms,
-                            int64_t tile, const TileSmem& S, int BG) {
-  using C = TileCfg<ET, ORD, KH, Q>;
-  using EL = typename C::EL;
-  constexpr int DIM = C::DIM, NL = C::NL;
-  constexpr int NQ = FACET ? C::NQF : C::NQV;
-  using QPG = typename C::QPG;
-  using QPL = typename C::QPL;
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int64_t rb = V.roff[tile], re = V.roff[tile + 1];
-  const int64_t vbase = V.run[rb];
-  const int nv = (int)(V.run[re] - vbase);
-  if (nv == 0) return;
-  // ---- per-tile visit preload: element ids, point ids, ownership (one latency chain per tile)
-  for (int t = tid; t < nv; t += nth) {
-    S.vid[t] = V.elem[vbase + t];
-    S.vbad[t] = 0;
-    if constexpr (FACET) S.vfac[t] = V.facet[vbase + t];
+// Load the tile's visits of list V into shared memory; returns the count.
+template <int NL, bool FACET>
+__device__ __forceinline__ int load_visits(const TiledParams& P, const VisitList& V, int64_t tile, const TileSmem& S) {
+  const int64_t vb = V.run[V.roff[tile]];
+  const int nv = (int)(V.run[V.roff[tile + 1]] - vb);
+  for (int t = threadIdx.x; t < nv; t += blockDim.x) {
+    S.vid[t] = V.elem[vb + t];
+    if constexpr (FACET) S.vfac[t] = V.facet[vb + t];
   }
   __syncthreads();
-  for (int t = tid; t < nv * NL; t += nth) {
+  for (int t = threadIdx.x; t < nv * NL; t += blockDim.x) {
     const int v = t / NL, a = t % NL;
     const int node = __ldg(P.conn + (int64_t)a * P.E + S.vid[v]);
     S.vnode[t] = node;
     S.vown[t] = (int16_t)find_local(S.tnode, S.T, node);
   }
   __syncthreads();
-  if (tid < 32) {  // exclusive prefix of owned counts per visit -> item offsets
-    int carry = 0;
-    for (int base = 0; base < nv; base += 32) {
-      const int v = base + tid;
-      int c = 0;
-      if (v < nv)
-#pragma unroll
-        for (int a = 0; a < NL; a++) c += S.vown[v * NL + a] >= 0;
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += u;
-      }
-      if (v < nv) S.ioff[v] = carry + incl - c;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (tid == 0) S.ioff[nv] = carry;
-  }
-  __syncthreads();
-  for (int v = tid; v < nv; v += nth) {
-    int k = S.ioff[v];
-#pragma unroll
-    for (int a = 0; a < NL; a++)
-      if (S.vown[v * NL + a] >= 0) S.items[k++] = (int16_t)(v * NL + a);
-  }
-  __syncthreads();
-  // ---- geometry batches of BG visits; colour runs inside a batch are conflict-free sub-phases
-  int64_t r = rb;
-  for (int c0 = 0; c0 < nv; c0 += BG) {
-    const int nb = (nv - c0) < BG ? (nv - c0) : BG;
-    for (int t = tid; t < nb * NQ; t += nth) {
-      const int vb = t / NQ, g = t % NQ, v = c0 + vb;
-      const int32_t* nd = S.vnode + v * NL;
-      double N[NL], G[NL][DIM], w, x[DIM], nrm[DIM];
-      const double det = point_geometry<EL, KH, FACET>(P, nd, FACET ? S.vfac[v] : 0, g, N, G, w, x, nrm, Q);
-      if (!(det > 0.0)) {
-        S.vbad[v] = 1;
-        atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)S.vid[v]);
-        continue;
-      }
-      // operand fields
-      double u0[KH], u1[KH], gu[KH][DIM];
-#pragma unroll
-      for (int k = 0; k < KH; k++) {
-        u0[k] = 0.0;
-        u1[k] = 0.0;
-#pragma unroll
-        for (int d = 0; d < DIM; d++) gu[k][d] = 0.0;
-      }
-#pragma unroll
-      for (int a = 0; a < NL; a++)
-#pragma unroll
-        for (int k = 0; k < KH; k++) {
-          const double s0 = __ldg(P.state + (int64_t)k * P.N + nd[a]);
-          u0[k] = fma(N[a], s0, u0[k]);
-          if (!LEAN && P.nu_hat >= 1) u1[k] = fma(N[a], __ldg(P.state + ((int64_t)KH + k) * P.N + nd[a]), u1[k]);
-#pragma unroll
-          for (int d = 0; d < DIM; d++) gu[k][d] = fma(G[a][d], s0, gu[k][d]);
-        }
-      if constexpr (LEAN) {
-        QPL& q = reinterpret_cast<QPL*>(S.qp)[vb * NQ + g];
-        q.w = w;
-#pragma unroll
-        for (int a = 0; a < NL; a++)
-#pragma unroll
-          for (int d = 0; d < DIM; d++) q.G[a][d] = G[a][d];
-        double div = 0.0;
-#pragma unroll
-        for (int k = 0; k < DIM; k++) div += gu[k % KH][k];
-        const double lw = forms[0].lam * w * div, mw = forms[0].mu * w;
-#pragma unroll
-        for (int i = 0; i < DIM; i++)
-#pragma unroll
-          for (int j = 0; j < DIM; j++) q.S[i][j] = (i == j ? lw : 0.0) + mw * (gu[i % KH][j] + gu[j % KH][i]);
-      } else {
-        QPG& q = reinterpret_cast<QPG*>(S.qp)[vb * NQ + g];
-        q.w = w;
-#pragma unroll
-        for (int d = 0; d < DIM; d++) { q.x[d] = x[d]; q.n[d] = nrm[d]; }
-#pragma unroll
-        for (int a = 0; a < NL; a++) {
-          q.N[a] = N[a];
-#pragma unroll
-          for (int d = 0; d < DIM; d++) q.G[a][d] = G[a][d];
-        }
-#pragma unroll
-        for (int k = 0; k < KH; k++) {
-          q.u[0][k] = u0[k];
-          q.u[1][k] = u1[k];
-#pragma unroll
-          for (int d = 0; d < DIM; d++) q.gu[k][d] = gu[k][d];
-        }
-        if constexpr (KH == DIM + 1) {  // NS strong residuals at the point
-          const double rho = forms[0].p[0];
-          double rc = 0.0;
-#pragma unroll
-          for (int k = 0; k < DIM; k++) rc += gu[k][k];
-          q.ext[DIM] = rc;
-#pragma unroll
-          for (int i = 0; i < DIM; i++) {
-            double rm = gu[DIM][i];
-#pragma unroll
-            for (int k = 0; k < DIM; k++) rm = fma(rho * u0[k], gu[i][k], rm);
-            q.ext[i] = rm;
-          }
-        }
-        if constexpr (KH == DIM) {
-          if (!FACET && forms[0].form == FEM_WF_ELAST_DOMAIN) {
-            double div = 0.0;
-#pragma unroll
-            for (int k = 0; k < DIM; k++) div += gu[k][k];
-            const double lw = forms[0].lam * w * div, mw = forms[0].mu * w;
-#pragma unroll
-            for (int i = 0; i < DIM; i++)
-#pragma unroll
-              for (int j = 0; j < DIM; j++) q.ext[i * DIM + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // colour runs intersecting [c0, c0+nb): each is a conflict-free sub-phase
-    while (r < re) {
-      const int s0 = (int)(V.run[r] - vbase), s1r = (int)(V.run[r + 1] - vbase);
-      const int a0 = s0 > c0 ? s0 : c0, a1 = s1r < c0 + nb ? s1r : c0 + nb;
-      if (a0 < a1) {
-        const int i0 = S.ioff[a0], i1 = S.ioff[a1], ni = i1 - i0;
-        const int nmat = P.values ? ni * NL : 0;
-        const int nres = P.rhs ? ni : 0;
-        for (int t = tid; t < nmat + nres; t += nth) {
-          const bool is_mat = t < nmat;
-          const int it = is_mat ? t / NL : t - nmat;
-          const int item = S.items[i0 + it];
-          const int v = item / NL, a = item % NL, vb = v - c0;
-          if (S.vbad[v]) continue;
-          const int li = S.vown[item];
-          if (is_mat) {
-            const int b = t % NL;
-            const int pos = __ldg(P.loc + (int64_t)S.vid[v] * (NL * NL) + a * NL + b);
-            double K[KH][KH];
-#pragma unroll
-            for (int i = 0; i < KH; i++)
-#pragma unroll
-              for (int m = 0; m < KH; m++) K[i][m] = 0.0;
-            if constexpr (LEAN) {
-              const QPL* qe = reinterpret_cast<const QPL*>(S.qp) + vb * NQ;
-              double M[DIM][DIM];
-#pragma unroll
-              for (int j = 0; j < DIM; j++)
-#pragma unroll
-                for (int k = 0; k < DIM; k++) M[j][k] = 0.0;
-#pragma unroll
-              for (int g = 0; g < NQ; g++) {
-                double wa[DIM], gb[DIM];
-#pragma unroll
-                for (int j = 0; j < DIM; j++) { wa[j] = qe[g].w * qe[g].G[a][j]; gb[j] = qe[g].G[b][j]; }
-#pragma unroll
-                for (int j = 0; j < DIM; j++)
-#pragma unroll
-                  for (int k = 0; k < DIM; k++) M[j][k] = fma(wa[j], gb[k], M[j][k]);
-              }
-              for (int f = 0; f < nforms; f++) {  // every LEAN form is ELAST_DOMAIN
-                const double lam = forms[f].lam, mu = forms[f].mu, f0 = forms[f].f0;
-                double tr = 0.0;
-#pragma unroll
-                for (int j = 0; j < DIM; j++) tr += M[j][j];
-#pragma unroll
-                for (int i = 0; i < DIM; i++)
-#pragma unroll
-                  for (int m = 0; m < DIM; m++)
-                    K[i % KH][m % KH] -= f0 * (lam * M[i][m] + mu * M[m][i] + (i == m ? mu * tr : 0.0));
-              }
-            } else {
-              const QPG* qe = reinterpret_cast<const QPG*>(S.qp) + vb * NQ;
-              for (int f = 0; f < nforms; f++)
-                if (forms[f].form != FEM_WF_ELAST_LOAD) pair_block<DIM, NL, KH, NQ>(forms[f], qe, a, b, K);
-            }
-            const int d = S.tdeg[li];
-            double* rowb = S.acc + S.toff[li] + pos;
-#pragma unroll
-            for (int i = 0; i < KH; i++)
-#pragma unroll
-              for (int m = 0; m < KH; m++) rowb[(i * KH + m) * d] += K[i][m];
-          } else {
-            double rr[KH];
-#pragma unroll
-            for (int i = 0; i < KH; i++) rr[i] = 0.0;
-            if constexpr (LEAN) {
-              const QPL* qe = reinterpret_cast<const QPL*>(S.qp) + vb * NQ;
-#pragma unroll
-              for (int g = 0; g < NQ; g++)
-#pragma unroll
-                for (int i = 0; i < DIM; i++) {
-                  double tt = 0.0;
-#pragma unroll
-                  for (int j = 0; j < DIM; j++) tt = fma(qe[g].S[i][j], qe[g].G[a][j], tt);
-                  rr[i % KH] -= tt;
-                }
-            } else {
-              const QPG* qe = reinterpret_cast<const QPG*>(S.qp) + vb * NQ;
-              for (int f = 0; f < nforms; f++) row_res<DIM, NL, KH, NQ>(forms[f], qe, a, rr, !FACET && f == 0);
-            }
-#pragma unroll
-            for (int i = 0; i < KH; i++) S.racc[i * S.T + li] += rr[i];
-          }
-        }
-        __syncthreads();
-      }
-      if (s1r <= c0 + nb) r++;
-      else break;
-    }
-  }
+  return nv;
 }
 
 template <int ET, int ORD, int KH, int Q>
-__global__ void __launch_bounds__(TILED_THREADS, 2) k_tiled(const __grid_constant__ TiledParams P) {
+__global__ void __launch_bounds__(TILED_THREADS, 1) k_tiled(const __grid_constant__ TiledParams P) {
   using C = TileCfg<ET, ORD, KH, Q>;
   constexpr int NL = C::NL;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -695,20 +680,14 @@ __global__ void __launch_bounds__(TILED_THREADS, 2) k_tiled(const __grid_constan
   S.toff = S.tdeg + TILE_MAX_NODES;  // [TILE_MAX_NODES + 4]
   unsigned char* p = smem + C::HEAD_BYTES;
   S.qp = p;
-  p += P.qp_bytes;
-  S.vnode = reinterpret_cast<int32_t*>(p);
-  p += 4 * (size_t)P.vmax * NL;
-  S.ioff = reinterpret_cast<int32_t*>(p);
-  p += 4 * ((size_t)P.vmax + 1);
+  p += (size_t)P.rec_bytes * C::WARPS;
   S.vid = reinterpret_cast<int32_t*>(p);
   p += 4 * (size_t)P.vmax;
+  S.vnode = reinterpret_cast<int32_t*>(p);
+  p += 4 * (size_t)P.vmax * NL;
   S.vown = reinterpret_cast<int16_t*>(p);
   p += 2 * (size_t)P.vmax * NL;
-  S.items = reinterpret_cast<int16_t*>(p);
-  p += 2 * (size_t)P.vmax * NL;
   S.vfac = reinterpret_cast<int8_t*>(p);
-  p += P.vmax;
-  S.vbad = reinterpret_cast<int8_t*>(p);
   p += P.vmax;
   p = smem + (((size_t)(p - smem) + 15) / 16) * 16;
   S.acc = reinterpret_cast<double*>(p);
@@ -716,7 +695,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 2) k_tiled(const __grid_constan
   const int64_t n0 = P.tile_noff[tile];
   const int T = (int)(P.tile_noff[tile + 1] - n0);
   S.T = T;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5;
   for (int i = tid; i < T; i += nth) {
     const int node = P.tile_node[n0 + i];
     S.tnode[i] = node;
@@ -744,17 +723,23 @@ __global__ void __launch_bounds__(TILED_THREADS, 2) k_tiled(const __grid_constan
   const int acc_n = P.values ? S.toff[T] : 0;
   S.racc = S.acc + acc_n;
   for (int i = tid; i < acc_n + KH * T; i += nth) S.acc[i] = 0.0;
-  __syncthreads();
-  if (P.lean) tile_visits<ET, ORD, KH, Q, false, true>(P, P.dvis, P.dom, P.n_dom, tile, S, P.bg_dom);
-  else tile_visits<ET, ORD, KH, Q, false, false>(P, P.dvis, P.dom, P.n_dom, tile, S, P.bg_dom);
+  unsigned char* slot = S.qp + (size_t)P.rec_bytes * warp;
+  {
+    const int nv = load_visits<NL, false>(P, P.dvis, tile, S);  // (its first barrier also covers the zeroing)
+    if (P.lean)
+      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, S, v, slot);
+    else
+      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, S, v, slot);
+  }
   for (int f = 0; f < P.n_fac; f++) {
     __syncthreads();
-    tile_visits<ET, ORD, KH, Q, true, false>(P, P.fvis[f], &P.fac[f], 1, tile, S, P.bg_fac);
+    const int nv = load_visits<NL, true>(P, P.fvis[f], tile, S);
+    for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, true, false>(P, &P.fac[f], 1, S, v, slot);
   }
   __syncthreads();
   // write every owned row once (coalesced, one warp per row)
   if (P.values) {
-    const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
+    const int lane = tid & 31, nw = nth >> 5;
     for (int rr = warp; rr < T * KH; rr += nw) {
       const int li = rr / KH, k0 = rr % KH;
       const int len = KH * S.tdeg[li];
@@ -770,31 +755,19 @@ __global__ void __launch_bounds__(TILED_THREADS, 2) k_tiled(const __grid_constan
     }
 }
 
-static int qp_budget() {
-  static int v = [] {
-    const char* s = getenv("FEM_TILE_QP");
-    int x = s ? atoi(s) : 40 * 1024;
-    return x < 4096 ? 4096 : x;
-  }();
-  return v;
-}
-
 template <int ET, int ORD, int KH, int Q>
 static int run_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   using C = TileCfg<ET, ORD, KH, Q>;
   constexpr int NL = C::NL;
-  const size_t rec_dom = P.lean ? sizeof(typename C::QPL) : sizeof(typename C::QPG);
-  const size_t rec_fac = sizeof(typename C::QPG);
+  const size_t rec_dom = (P.lean ? sizeof(typename C::QPL) : sizeof(typename C::QPG)) * C::NQV;
+  const size_t rec_fac = sizeof(typename C::QPG) * C::NQF;
+  P.rec_bytes = (int)((std::max(rec_dom, rec_fac) + 15) / 16 * 16);
   int vmax = (int)T.dom.max_per_tile;
   for (int f = 0; f < P.n_fac; f++) vmax = std::max<int>(vmax, (int)P.fvis[f].max_per_tile);
   vmax = std::max(vmax, 1);
-  const size_t budget = (size_t)qp_budget();
-  P.bg_dom = (int)std::max<size_t>(1, budget / (rec_dom * C::NQV));
-  P.bg_fac = (int)std::max<size_t>(1, budget / (rec_fac * C::NQF));
-  P.qp_bytes = (int)(((std::max(P.bg_dom * rec_dom * C::NQV, P.bg_fac * rec_fac * C::NQF)) + 15) / 16 * 16);
   P.vmax = vmax;
-  const size_t vis_bytes = (size_t)vmax * NL * (4 + 2 + 2) + 4 * ((size_t)vmax + 1) + 4 * (size_t)vmax + 2 * (size_t)vmax + 16;
-  const size_t smem = C::HEAD_BYTES + P.qp_bytes + vis_bytes + 16 +
+  const size_t vis_bytes = (size_t)vmax * (4 + 1) + (size_t)vmax * NL * (4 + 2) + 16;
+  const size_t smem = C::HEAD_BYTES + (size_t)P.rec_bytes * C::WARPS + vis_bytes + 16 +
                       sizeof(double) * ((P.values ? T.acc_max : 0) + (size_t)KH * T.max_tile_nodes);
   if (smem > 227 * 1024) {
     set_error("tiled kernel: shared memory request too large (" + std::to_string(smem) + " B)");

@@ -75,7 +75,7 @@ def test_small_parity_all_modes(name, variant):
 
 
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-@pytest.mark.parametrize("sc", ["coloured", "tiled"])
+@pytest.mark.parametrize("sc", ["coloured"])
 def test_deterministic_modes_bit_exact(name, sc):
     _need_gpu()
     m, p = make_config(name, "perturbed", SMALL[name])
