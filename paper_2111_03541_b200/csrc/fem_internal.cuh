@@ -54,6 +54,9 @@ struct TileSchedule {
   std::vector<VisitList> bnd;    // facet visits per boundary set
   uint8_t* loc = nullptr;        // device [E][n_loc][n_loc]: slot - rowptr_s[α(e,a)] (255: not owned)
   int64_t visits_total = 0;
+  int64_t* halo_off = nullptr;   // device [n_tiles+1]: points of the elements a tile visits
+  int32_t* halo_node = nullptr;  // device: sorted per tile
+  int64_t max_halo = 0;
 };
 
 }  // namespace fem

@@ -1,0 +1,340 @@
+// hex_tiled.cu — the c5/c2 hot path: Q1 hexahedra, 2x2x2 Gauss-Legendre points, node-tile owner
+// gather (see tiled.cu) with a warp-synchronous element visit built around fp64 tensor-core MMA.
+//
+// PAPER.md D-3 for the elasticity form -(ε_ij, σ_ij) gives per element
+//   K_(a,i),(b,m) = -f0 Σ_γ w [λ G_ai G_bm + μ G_am G_bi + μ δ_im G_a·G_b]
+//                 = -f0 (λ M^im_ab + μ M^mi_ab + μ δ_im tr M_ab),   M^jk_ab = Σ_γ w_γ G_aj(γ) G_bk(γ),
+// and for the thermal form -k(T_,i,T_,i) - C(T,T_t) K_ab = -k f0 Σ_j M^jj_ab - C f1 Σ_γ w N_a N_b.
+// Lane l = 4a + c of a warp holds node a's gradient at Gauss points c and c+4, which is exactly the
+// operand layout of mma.m8n8k4.f64 (A: row = l>>2, col = l&3; B: row = l&3, col = l>>2), so each 8x8
+// tile M^jk (rows a, columns b) is two DMMA with the lane's own registers as A and B fragments; the
+// accumulator fragment leaves lane l with M^jk_(a, 2c), M^jk_(a, 2c+1): the full 3x3 block of two pairs.
+// The geometry (J, det J, J^-1 and the operand gradients) is computed with lane groups of
+// 4 per Gauss point and shuffled to the fragment layout.  Visits are processed colour-synchronously
+// (elements of one colour share no point), so the shared-memory accumulator takes plain adds and the
+// result is bit-identical run to run.  Boundary terms reuse the generic warp path (tiled.cuh).
+#include <algorithm>
+#include <string>
+
+#include "tiled.cuh"
+
+namespace fem {
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Q1 shape value and reference gradient of node a at Gauss point q = ix + 2 iy + 4 iz (ξ = ±1/√3).
+__device__ __forceinline__ void hex_ref(int a, int q, double (&g)[3], double& N) {
+  const double r = 0.57735026918962576451;
+  const double sx = hex_sign(a, 0), sy = hex_sign(a, 1), sz = hex_sign(a, 2);
+  const double fx = 0.5 * (1.0 + sx * ((q & 1) ? r : -r));
+  const double fy = 0.5 * (1.0 + sy * ((q & 2) ? r : -r));
+  const double fz = 0.5 * (1.0 + sz * ((q & 4) ? r : -r));
+  N = fx * fy * fz;
+  g[0] = 0.5 * sx * fy * fz;
+  g[1] = 0.5 * sy * fx * fz;
+  g[2] = 0.5 * sz * fx * fy;
+}
+
+__device__ __forceinline__ double sum4(double v) {  // over the 4 lanes of a group (xor 1, 2)
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+struct HexCoef {  // combined coefficients of the batch's domain forms
+  double cl, cm;   // Σ f0 λ, Σ f0 μ            (elasticity matrix)
+  double sl, sm;   // Σ λ, Σ μ                  (elasticity residual)
+  double kf0, Cf1; // Σ k f0, Σ C f1            (thermal matrix)
+};
+
+template <int KH, bool DET>
+__device__ __forceinline__ void hex_visit(const TiledParams& P, const TileSmem& S, const HexCoef& H, int v) {
+  const int lane = threadIdx.x & 31;
+  const int16_t* own = S.vown + v * 8;
+  const int e = S.vid[v];
+  // ---- stage G: Gauss point q = lane >> 2, nodes sub and sub + 4
+  const int q = lane >> 2, sub = lane & 3;
+  double J[3][3], Dr[KH][3], xq[3] = {0, 0, 0}, Tt = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) J[i][j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < KH; k++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) Dr[k][j] = 0.0;
+  const int16_t* hv = S.vhal + v * 8;
+  const int HH = S.H;
+#pragma unroll
+  for (int t = 0; t < 2; t++) {
+    const int a = sub + 4 * t, h = hv[a];
+    double g[3], N;
+    hex_ref(a, q, g, N);
+    double X[3];
+#pragma unroll
+    for (int d = 0; d < 3; d++) X[d] = S.hdat[d * HH + h];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) J[i][j] = fma(X[i], g[j], J[i][j]);
+#pragma unroll
+    for (int k = 0; k < KH; k++) {
+      const double D = S.hdat[(3 + k) * HH + h];
+#pragma unroll
+      for (int j = 0; j < 3; j++) Dr[k][j] = fma(D, g[j], Dr[k][j]);
+    }
+    if constexpr (KH == 1) {
+#pragma unroll
+      for (int d = 0; d < 3; d++) xq[d] = fma(N, X[d], xq[d]);
+      if (P.nu_hat >= 1) Tt = fma(N, S.hdat[(3 + KH) * HH + h], Tt);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) J[i][j] = sum4(J[i][j]);
+#pragma unroll
+  for (int k = 0; k < KH; k++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) Dr[k][j] = sum4(Dr[k][j]);
+  if constexpr (KH == 1) {
+#pragma unroll
+    for (int d = 0; d < 3; d++) xq[d] = sum4(xq[d]);
+    Tt = sum4(Tt);
+  }
+  const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+  if (__any_sync(0xffffffffu, !(det > 0.0))) {
+    if (lane == 0) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)e);
+    return;
+  }
+  const double rr = 1.0 / det;
+  double Ji[3][3];
+  Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+  const double w = det;  // Gauss-Legendre weight 1 per point
+  // operand gradients ∇φ = Dr J^{-1}; point coefficients of the residual
+  double Sq[3][3];  // elasticity: w σ_ij;  thermal: Sq[0][i] = w k ∇T_i, Sq[1][0] = w (s - C Ṫ)
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+#pragma unroll
+    for (int i = 0; i < 3; i++) Sq[k][i] = 0.0;
+  if constexpr (KH == 3) {
+    double gu[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+#pragma unroll
+      for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+    const double lw = H.sl * w * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * w;
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) Sq[i][j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+  } else {
+    double gT[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) gT[i] = Dr[0][0] * Ji[0][i] + Dr[0][1] * Ji[1][i] + Dr[0][2] * Ji[2][i];
+    double kk = 0.0, cn = 0.0;
+    for (int f = 0; f < P.n_dom; f++) {
+      const FormArgs& F = P.dom[f];
+      double s = F.p[2];
+      if (F.p[3] != 0.0) s *= sin(M_PI * xq[0]) * sin(M_PI * xq[1]) * sin(M_PI * xq[2]);
+      kk += F.p[1];
+      cn += s - (P.nu_hat >= 1 ? F.p[0] * Tt : 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; i++) Sq[0][i] = w * kk * gT[i];
+    Sq[1][0] = w * cn;
+  }
+  // ---- fragment layout: node a = lane >> 2, Gauss points c and c + 4
+  const int a = lane >> 2, c = lane & 3;
+  const int s0 = 4 * c, s1 = 4 * c + 16;  // lanes holding points c and c+4 in the stage-G layout
+  double G0[3], G1[3], N0, N1, g0[3], g1[3];
+  hex_ref(a, c, g0, N0);
+  hex_ref(a, c + 4, g1, N1);
+  double w0 = __shfl_sync(0xffffffffu, w, s0), w1 = __shfl_sync(0xffffffffu, w, s1);
+#pragma unroll
+  for (int i = 0; i < 3; i++) { G0[i] = 0.0; G1[i] = 0.0; }
+#pragma unroll
+  for (int j = 0; j < 3; j++)
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const double j0 = __shfl_sync(0xffffffffu, Ji[j][i], s0), j1 = __shfl_sync(0xffffffffu, Ji[j][i], s1);
+      G0[i] = fma(j0, g0[j], G0[i]);
+      G1[i] = fma(j1, g1[j], G1[i]);
+    }
+  const int li = own[a];
+  // ---- residual rows (D-2): r_a = -Σ_γ w σ G_a (elasticity) | Σ_γ [N_a w(s - CṪ) - G_a·(w k ∇T)]
+  if (P.rhs) {
+    double r[KH];
+    if constexpr (KH == 3) {
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          t = fma(__shfl_sync(0xffffffffu, Sq[i][j], s0), G0[j], t);
+          t = fma(__shfl_sync(0xffffffffu, Sq[i][j], s1), G1[j], t);
+        }
+        r[i] = -sum4(t);
+      }
+    } else {
+      double t = N0 * __shfl_sync(0xffffffffu, Sq[1][0], s0) + N1 * __shfl_sync(0xffffffffu, Sq[1][0], s1);
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        t = fma(-G0[j], __shfl_sync(0xffffffffu, Sq[0][j], s0), t);
+        t = fma(-G1[j], __shfl_sync(0xffffffffu, Sq[0][j], s1), t);
+      }
+      r[0] = sum4(t);
+    }
+    if (c == 0 && li >= 0) {
+#pragma unroll
+      for (int i = 0; i < KH; i++) {
+        if constexpr (DET) S.racc[i * S.T + li] += r[i];
+        else atomicAdd(S.racc + i * S.T + li, r[i]);
+      }
+    }
+  }
+  // ---- tangent (D-3): Gram tiles on the fp64 tensor cores
+  if (P.values) {
+    double Kb[2][KH][KH];
+    if constexpr (KH == 3) {
+      double M[3][3][2];
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          M[j][k][0] = 0.0;
+          M[j][k][1] = 0.0;
+          dmma884(M[j][k], w0 * G0[j], G0[k]);
+          dmma884(M[j][k], w1 * G1[j], G1[k]);
+        }
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) Kb[t][i][m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+      }
+    } else {
+      double M[2] = {0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        dmma884(M, w0 * G0[j], G0[j]);
+        dmma884(M, w1 * G1[j], G1[j]);
+      }
+      double Mm[2] = {0.0, 0.0};
+      if (H.Cf1 != 0.0) {
+        dmma884(Mm, w0 * N0, N0);
+        dmma884(Mm, w1 * N1, N1);
+      }
+#pragma unroll
+      for (int t = 0; t < 2; t++) Kb[t][0][0] = -(H.kf0 * M[t] + H.Cf1 * Mm[t]);
+    }
+    if (li >= 0) {
+      const int d = S.tdeg[li];
+      double* base = S.acc + S.toff[li];
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const int b = 2 * c + t;
+        double* rowb = base + __ldg(P.loc + (int64_t)e * 64 + a * 8 + b);
+#pragma unroll
+        for (int i = 0; i < KH; i++)
+#pragma unroll
+          for (int m = 0; m < KH; m++) {
+            if constexpr (DET) rowb[(i * KH + m) * d] += Kb[t][i][m];
+            else atomicAdd(rowb + (i * KH + m) * d, Kb[t][i][m]);
+          }
+      }
+    }
+  }
+}
+
+template <int KH, bool DET>
+__global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_tiled(const __grid_constant__ TiledParams P) {
+  using C = TileCfg<ET_HEX, 1, KH, 2>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  TileSmem S = tile_smem_layout<8>(smem, P, C::WARPS);
+  const int64_t tile = blockIdx.x;
+  tile_prologue<KH>(P, S, tile);
+  HexCoef H = {0, 0, 0, 0, 0, 0};
+  for (int f = 0; f < P.n_dom; f++) {
+    const FormArgs& F = P.dom[f];
+    H.cl += F.f0 * F.lam; H.cm += F.f0 * F.mu; H.sl += F.lam; H.sm += F.mu;
+    H.kf0 += F.p[1] * F.f0;
+    if (F.nu_hat >= 1) H.Cf1 += F.p[0] * F.f1;
+  }
+  const int warp = threadIdx.x >> 5;
+  __syncthreads();
+  load_halo<3>(P, S, tile);
+  const int nv = load_visits<8, false>(P, P.dvis, tile, S);
+  if constexpr (DET) {
+    const int64_t rb = P.dvis.roff[tile], re = P.dvis.roff[tile + 1];
+    const int64_t vbase = P.dvis.run[rb];
+    for (int64_t r = rb; r < re; r++) {  // colour runs: conflict-free, plain shared-memory adds
+      const int v0 = (int)(P.dvis.run[r] - vbase), v1 = (int)(P.dvis.run[r + 1] - vbase);
+      for (int v = v0 + warp; v < v1; v += C::WARPS) hex_visit<KH, true>(P, S, H, v);
+      __syncthreads();
+    }
+  } else {  // warps flow freely; shared-memory fp64 atomics resolve the rare conflicts
+    for (int v = warp; v < nv; v += C::WARPS) hex_visit<KH, false>(P, S, H, v);
+  }
+  unsigned char* slot = S.qp + (size_t)P.rec_bytes * warp;
+  tile_facets<ET_HEX, 1, KH, 2>(P, S, tile, slot);
+  tile_epilogue<KH>(P, S);
+}
+
+template <int KH, bool DET>
+static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
+  using C = TileCfg<ET_HEX, 1, KH, 2>;
+  P.rec_bytes = (int)((sizeof(typename C::QPG) * C::NQF + 15) / 16 * 16);
+  int vmax = (int)T.dom.max_per_tile;
+  for (int f = 0; f < P.n_fac; f++) vmax = std::max<int>(vmax, (int)P.fvis[f].max_per_tile);
+  P.vmax = std::max(vmax, 1);
+  P.hmax = (int)std::max<int64_t>(T.max_halo, 1);
+  P.hcomp = 3 + KH * (P.nu_hat >= 1 ? 2 : 1);
+  P.halo_off = T.halo_off;
+  P.halo_node = T.halo_node;
+  const size_t vis_bytes = (size_t)P.vmax * (4 + 1) + (size_t)P.vmax * 8 * (4 + 2 + 2) + 32;
+  const size_t halo_bytes = ((4 * (size_t)P.hmax + 15) / 16) * 16 + 8 * (size_t)P.hmax * P.hcomp;
+  const size_t uni = std::max(halo_bytes, (size_t)P.rec_bytes * C::WARPS) + 16;
+  const size_t smem = C::HEAD_BYTES + uni + vis_bytes + 16 +
+                      sizeof(double) * ((P.values ? T.acc_max : 0) + (size_t)KH * T.max_tile_nodes);
+  if (smem > 227 * 1024) {
+    set_error("hex tiled kernel: shared memory request too large (" + std::to_string(smem) + " B)");
+    return FEM_E_UNSUPPORTED;
+  }
+  FEM_CUDA_TRY(cudaFuncSetAttribute(k_hex_tiled<KH, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (T.n_tiles <= 0) return 0;
+  k_hex_tiled<KH, DET><<<(unsigned)T.n_tiles, TILED_THREADS, smem, s>>>(P);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Q1 hex, 2x2x2 points, domain terms all ELAST_DOMAIN (κ̂ = 3) or all THERMAL_DOMAIN (κ̂ = 1).
+int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled) {
+  *handled = false;
+  if (P.n_dom == 0) return 0;
+  for (int f = 0; f < P.n_dom; f++) {
+    if (kh == 3 && P.dom[f].form != FEM_WF_ELAST_DOMAIN) return 0;
+    if (kh == 1 && P.dom[f].form != FEM_WF_THERMAL_DOMAIN) return 0;
+  }
+  if (kh != 1 && kh != 3) return 0;
+  *handled = true;
+  if (det) return kh == 3 ? run_hex<3, true>(P, T, s) : run_hex<1, true>(P, T, s);
+  return kh == 3 ? run_hex<3, false>(P, T, s) : run_hex<1, false>(P, T, s);
+}
+
+}  // namespace fem

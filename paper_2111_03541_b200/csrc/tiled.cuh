@@ -1,0 +1,526 @@
+// tiled.cuh — shared pieces of the node-tile owner-gather kernels (tiled.cu, hex_tiled.cu).
+#pragma once
+#include <cstdint>
+
+#include "blocks.cuh"
+#include "elements.cuh"
+#include "fem_internal.cuh"
+
+namespace fem {
+
+constexpr int TILE_MAX_NODES = 512;
+constexpr int MAX_DOM_TERMS = 4;
+constexpr int MAX_FAC_TERMS = 8;
+constexpr int TILED_THREADS = 512;
+
+// ------------------------------------------------------------------ device: the tiled kernel
+struct TiledParams {
+  int n_dom, n_fac, lean;
+  FormArgs dom[MAX_DOM_TERMS];
+  FormArgs fac[MAX_FAC_TERMS];
+  VisitList dvis;
+  VisitList fvis[MAX_FAC_TERMS];
+  const int64_t* tile_noff;
+  const int32_t* tile_node;
+  int64_t N, E, own_lo, n_own, nnz_s;
+  const double* coords;
+  const int32_t* conn;
+  const double* state;
+  const int64_t* rowptr_s;
+  const uint8_t* loc;
+  double* values;
+  double* rhs;
+  long long* err;
+  int nu_hat;
+  int vmax;      // capacity of the per-tile visit arrays
+  int rec_bytes; // bytes of one warp's point-record slot
+  const int64_t* halo_off;  // per tile: sorted points of the visited elements
+  const int32_t* halo_node;
+  int hmax;      // capacity of the halo arrays (0: halo staging off)
+  int hcomp;     // doubles per halo point: dim coords + κ̂·(ν̂+1) state values
+};
+
+// Lean point record for elasticity-only domain visits: w, ∇N_a, and w·σ.
+template <int DIM, int NL>
+struct QPE {
+  double w;
+  double G[NL][DIM];
+  double S[DIM][DIM];
+};
+
+template <int ET, int ORD, int KH, int Q>
+struct TileCfg {
+  using EL = Elem<ET, ORD>;
+  static constexpr int DIM = EL::DIM, NL = EL::NL;
+  static constexpr int NQV = EL::vol_nq(Q), NQF = EL::fac_nq(Q);
+  using QPG = QPX<DIM, NL, KH>;
+  using QPL = QPE<DIM, NL>;
+  static constexpr size_t HEAD_BYTES = 20 * TILE_MAX_NODES + 16;
+  static constexpr int WARPS = TILED_THREADS / 32;
+};
+
+// lanes per quadrature point in the cooperative geometry: largest power of two with NQ*NSUB <= 32
+template <int NQ>
+struct Sub {
+  static constexpr int v = NQ >= 32 ? 1 : (NQ * 32 <= 32 ? 32 : (NQ * 16 <= 32 ? 16 : (NQ * 8 <= 32 ? 8 :
+                           (NQ * 4 <= 32 ? 4 : (NQ * 2 <= 32 ? 2 : 1)))));
+};
+
+__device__ __forceinline__ int find_local(const int32_t* __restrict__ tnode, int T, int node) {
+  int lo = 0, hi = T - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = tnode[mid];
+    if (v == node) return mid;
+    if (v < node) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return -1;
+}
+
+template <int NSUB>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = 1; o < NSUB; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct TileSmem {
+  int32_t* tnode; int64_t* trps; int32_t* tdeg; int32_t* toff;
+  int32_t* vid;    // [vmax] element id of each visit
+  int8_t* vfac;    // [vmax] facet id
+  int32_t* vnode;  // [vmax*NL]
+  int16_t* vown;   // [vmax*NL] tile-local point index or -1
+  unsigned char* qp;  // per-warp point-record slots
+  int16_t* vhal;   // [vmax*NL] halo index of each visit point
+  int32_t* hnode;  // [hmax]
+  double* hdat;    // [hcomp][hmax] staged coordinates and state of the halo points
+  int H;
+  double* acc;
+  double* racc;
+  int T;
+};
+
+// One warp assembles one element (or facet) visit into the tile accumulator.
+template <int ET, int ORD, int KH, int Q, bool FACET, bool LEAN>
+__device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs* forms, int nforms, const TileSmem& S,
+                                           int v, unsigned char* slot) {
+  using C = TileCfg<ET, ORD, KH, Q>;
+  using EL = typename C::EL;
+  constexpr int DIM = C::DIM, NL = C::NL;
+  constexpr int NQ = FACET ? C::NQF : C::NQV;
+  constexpr int NSUB = Sub<NQ>::v;
+  using QPG = typename C::QPG;
+  using QPL = typename C::QPL;
+  const int lane = threadIdx.x & 31;
+  const int32_t* nd = S.vnode + v * NL;
+  const int16_t* own = S.vown + v * NL;
+  // ---- cooperative geometry: lane -> (point g, node group sub)
+  const int g = lane / NSUB, sub = lane % NSUB;
+  const bool gl = g < NQ;
+  const int gq = gl ? g : 0;
+  double xi[3] = {0, 0, 0}, wref, mref[3] = {0, 0, 0};
+  if constexpr (FACET) EL::fac_qp(Q, S.vfac[v], gq, xi, wref, mref);
+  else EL::vol_qp(Q, gq, xi, wref);
+  double N[NL], dN[NL][DIM];
+  EL::shape(xi, N, dN);
+  double J[DIM][DIM], xp[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; i++) {
+    xp[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < DIM; j++) J[i][j] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < NL; a++)
+    if (a % NSUB == sub) {
+      double X[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; d++) X[d] = __ldg(P.coords + (int64_t)d * P.N + nd[a]);
+#pragma unroll
+      for (int i = 0; i < DIM; i++) {
+        xp[i] = fma(N[a], X[i], xp[i]);
+#pragma unroll
+        for (int j = 0; j < DIM; j++) J[i][j] = fma(X[i], dN[a][j], J[i][j]);
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < DIM; i++) {
+    xp[i] = group_sum<NSUB>(xp[i]);
+#pragma unroll
+    for (int j = 0; j < DIM; j++) J[i][j] = group_sum<NSUB>(J[i][j]);
+  }
+  double Ji[DIM][DIM], det;
+  if constexpr (DIM == 2) {
+    det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double rr = 1.0 / det;
+    Ji[0][0] = J[1][1] * rr;  Ji[0][1] = -J[0][1] * rr;
+    Ji[1][0] = -J[1][0] * rr; Ji[1][1] = J[0][0] * rr;
+  } else {
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    const double rr = 1.0 / det;
+    Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+  }
+  const bool bad = __any_sync(0xffffffffu, gl && !(det > 0.0));
+  if (bad) {
+    if (lane == 0) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)S.vid[v]);
+    return;
+  }
+  double w, nrm[DIM];
+  if constexpr (FACET) {  // Nanson: n dA = det(J) J^{-T} m̂ dÂ
+    double nn = 0.0;
+#pragma unroll
+    for (int i = 0; i < DIM; i++) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < DIM; j++) sacc = fma(Ji[j][i], mref[j], sacc);
+      nrm[i] = det * sacc;
+      nn = fma(nrm[i], nrm[i], nn);
+    }
+    const double dA = sqrt(nn);
+#pragma unroll
+    for (int i = 0; i < DIM; i++) nrm[i] /= dA;
+    w = wref * dA;
+  } else {
+#pragma unroll
+    for (int i = 0; i < DIM; i++) nrm[i] = 0.0;
+    w = wref * det;
+  }
+  // gradients of this lane's nodes and partial operand fields
+  double u0[KH], u1[KH], gu[KH][DIM];
+#pragma unroll
+  for (int k = 0; k < KH; k++) {
+    u0[k] = 0.0;
+    u1[k] = 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; d++) gu[k][d] = 0.0;
+  }
+  QPL* ql = reinterpret_cast<QPL*>(slot);
+  QPG* qg = reinterpret_cast<QPG*>(slot);
+#pragma unroll
+  for (int a = 0; a < NL; a++)
+    if (a % NSUB == sub) {
+      double Ga[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; i++) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; j++) sacc = fma(Ji[j][i], dN[a][j], sacc);
+        Ga[i] = sacc;
+      }
+      if (gl) {
+        if constexpr (LEAN) {
+#pragma unroll
+          for (int i = 0; i < DIM; i++) ql[gq].G[a][i] = Ga[i];
+        } else {
+          qg[gq].N[a] = N[a];
+#pragma unroll
+          for (int i = 0; i < DIM; i++) qg[gq].G[a][i] = Ga[i];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KH; k++) {
+        const double s0 = __ldg(P.state + (int64_t)k * P.N + nd[a]);
+        u0[k] = fma(N[a], s0, u0[k]);
+        if (!LEAN && P.nu_hat >= 1) u1[k] = fma(N[a], __ldg(P.state + ((int64_t)KH + k) * P.N + nd[a]), u1[k]);
+#pragma unroll
+        for (int d = 0; d < DIM; d++) gu[k][d] = fma(Ga[d], s0, gu[k][d]);
+      }
+    }
+#pragma unroll
+  for (int k = 0; k < KH; k++) {
+    u0[k] = group_sum<NSUB>(u0[k]);
+    if (!LEAN) u1[k] = group_sum<NSUB>(u1[k]);
+#pragma unroll
+    for (int d = 0; d < DIM; d++) gu[k][d] = group_sum<NSUB>(gu[k][d]);
+  }
+  if (gl && sub == 0) {
+    if constexpr (LEAN) {
+      ql[gq].w = w;
+      double div = 0.0;
+#pragma unroll
+      for (int k = 0; k < DIM; k++) div += gu[k % KH][k];
+      const double lw = forms[0].lam * w * div, mw = forms[0].mu * w;
+#pragma unroll
+      for (int i = 0; i < DIM; i++)
+#pragma unroll
+        for (int j = 0; j < DIM; j++) ql[gq].S[i][j] = (i == j ? lw : 0.0) + mw * (gu[i % KH][j] + gu[j % KH][i]);
+    } else {
+      QPG& q = qg[gq];
+      q.w = w;
+#pragma unroll
+      for (int d = 0; d < DIM; d++) { q.x[d] = xp[d]; q.n[d] = nrm[d]; }
+#pragma unroll
+      for (int k = 0; k < KH; k++) {
+        q.u[0][k] = u0[k];
+        q.u[1][k] = u1[k];
+#pragma unroll
+        for (int d = 0; d < DIM; d++) q.gu[k][d] = gu[k][d];
+      }
+      if constexpr (KH == DIM + 1) {  // NS strong residuals at the point
+        const double rho = forms[0].p[0];
+        double rc = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; k++) rc += gu[k][k];
+        q.ext[DIM] = rc;
+#pragma unroll
+        for (int i = 0; i < DIM; i++) {
+          double rm = gu[DIM][i];
+#pragma unroll
+          for (int k = 0; k < DIM; k++) rm = fma(rho * u0[k], gu[i][k], rm);
+          q.ext[i] = rm;
+        }
+      }
+      if constexpr (KH == DIM) {
+        if (!FACET && forms[0].form == FEM_WF_ELAST_DOMAIN) {
+          double div = 0.0;
+#pragma unroll
+          for (int k = 0; k < DIM; k++) div += gu[k][k];
+          const double lw = forms[0].lam * w * div, mw = forms[0].mu * w;
+#pragma unroll
+          for (int i = 0; i < DIM; i++)
+#pragma unroll
+            for (int j = 0; j < DIM; j++) q.ext[i * DIM + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // ---- owned test nodes of this visit
+  int owned_a[NL], n_owned = 0;
+#pragma unroll
+  for (int a = 0; a < NL; a++)
+    if (own[a] >= 0) owned_a[n_owned++] = a;
+  const int npair = P.values ? n_owned * NL : 0;
+  const int nres = P.rhs ? n_owned : 0;
+  const int e = S.vid[v];
+  for (int t = lane; t < npair + nres; t += 32) {
+    const bool is_mat = t < npair;
+    const int ia = is_mat ? t / NL : t - npair;
+    int a = 0;
+#pragma unroll
+    for (int k = 0; k < NL; k++)
+      if (k == ia) a = owned_a[k];
+    const int li = own[a];
+    if (is_mat) {
+      const int b = t % NL;
+      const int pos = __ldg(P.loc + (int64_t)e * (NL * NL) + a * NL + b);
+      double K[KH][KH];
+#pragma unroll
+      for (int i = 0; i < KH; i++)
+#pragma unroll
+        for (int m = 0; m < KH; m++) K[i][m] = 0.0;
+      if constexpr (LEAN) {
+        double M[DIM][DIM];
+#pragma unroll
+        for (int j = 0; j < DIM; j++)
+#pragma unroll
+          for (int k = 0; k < DIM; k++) M[j][k] = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < NQ; gg++) {
+          double wa[DIM], gb[DIM];
+          const double wq = ql[gg].w;
+#pragma unroll
+          for (int j = 0; j < DIM; j++) { wa[j] = wq * ql[gg].G[a][j]; gb[j] = ql[gg].G[b][j]; }
+#pragma unroll
+          for (int j = 0; j < DIM; j++)
+#pragma unroll
+            for (int k = 0; k < DIM; k++) M[j][k] = fma(wa[j], gb[k], M[j][k]);
+        }
+        for (int f = 0; f < nforms; f++) {  // every LEAN form is ELAST_DOMAIN
+          const double lam = forms[f].lam, mu = forms[f].mu, f0 = forms[f].f0;
+          double tr = 0.0;
+#pragma unroll
+          for (int j = 0; j < DIM; j++) tr += M[j][j];
+#pragma unroll
+          for (int i = 0; i < DIM; i++)
+#pragma unroll
+            for (int m = 0; m < DIM; m++)
+              K[i % KH][m % KH] -= f0 * (lam * M[i][m] + mu * M[m][i] + (i == m ? mu * tr : 0.0));
+        }
+      } else {
+        for (int f = 0; f < nforms; f++)
+          if (forms[f].form != FEM_WF_ELAST_LOAD) pair_block<DIM, NL, KH, NQ>(forms[f], qg, a, b, K);
+      }
+      const int d = S.tdeg[li];
+      double* rowb = S.acc + S.toff[li] + pos;
+#pragma unroll
+      for (int i = 0; i < KH; i++)
+#pragma unroll
+        for (int m = 0; m < KH; m++) atomicAdd(rowb + (i * KH + m) * d, K[i][m]);
+    } else {
+      double rr[KH];
+#pragma unroll
+      for (int i = 0; i < KH; i++) rr[i] = 0.0;
+      if constexpr (LEAN) {
+#pragma unroll
+        for (int gg = 0; gg < NQ; gg++)
+#pragma unroll
+          for (int i = 0; i < DIM; i++) {
+            double tt = 0.0;
+#pragma unroll
+            for (int j = 0; j < DIM; j++) tt = fma(ql[gg].S[i][j], ql[gg].G[a][j], tt);
+            rr[i % KH] -= tt;
+          }
+      } else {
+        for (int f = 0; f < nforms; f++) row_res<DIM, NL, KH, NQ>(forms[f], qg, a, rr, !FACET && f == 0);
+      }
+#pragma unroll
+      for (int i = 0; i < KH; i++) atomicAdd(S.racc + i * S.T + li, rr[i]);
+    }
+  }
+  __syncwarp();
+}
+
+// Stage the tile's halo points (coordinates + state levels) in shared memory.
+template <int DIM>
+__device__ __forceinline__ void load_halo(const TiledParams& P, TileSmem& S, int64_t tile) {
+  const int64_t h0 = P.halo_off[tile];
+  const int H = (int)(P.halo_off[tile + 1] - h0);
+  S.H = H;
+  for (int i = threadIdx.x; i < H; i += blockDim.x) S.hnode[i] = P.halo_node[h0 + i];
+  __syncthreads();
+  const int ns = P.hcomp - DIM;
+  for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
+    const int c = t / H, i = t % H, node = S.hnode[i];
+    S.hdat[t] = c < DIM ? __ldg(P.coords + (int64_t)c * P.N + node) : __ldg(P.state + (int64_t)(c - DIM) * P.N + node);
+  }
+  (void)ns;
+}
+
+// Load the tile's visits of list V into shared memory; returns the count.
+template <int NL, bool FACET>
+__device__ __forceinline__ int load_visits(const TiledParams& P, const VisitList& V, int64_t tile, const TileSmem& S) {
+  const int64_t vb = V.run[V.roff[tile]];
+  const int nv = (int)(V.run[V.roff[tile + 1]] - vb);
+  for (int t = threadIdx.x; t < nv; t += blockDim.x) {
+    S.vid[t] = V.elem[vb + t];
+    if constexpr (FACET) S.vfac[t] = V.facet[vb + t];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nv * NL; t += blockDim.x) {
+    const int v = t / NL, a = t % NL;
+    const int node = __ldg(P.conn + (int64_t)a * P.E + S.vid[v]);
+    S.vnode[t] = node;
+    S.vown[t] = (int16_t)find_local(S.tnode, S.T, node);
+    if (P.hmax) S.vhal[t] = (int16_t)find_local(S.hnode, S.H, node);
+  }
+  __syncthreads();
+  return nv;
+}
+
+
+// shared-memory carve-up: head (tile points) | per-warp point records | visit arrays | accumulator
+template <int NL>
+__device__ __forceinline__ TileSmem tile_smem_layout(unsigned char* smem, const TiledParams& P, int warps) {
+  TileSmem S;
+  S.trps = reinterpret_cast<int64_t*>(smem);
+  S.tnode = reinterpret_cast<int32_t*>(S.trps + TILE_MAX_NODES);
+  S.tdeg = S.tnode + TILE_MAX_NODES;
+  S.toff = S.tdeg + TILE_MAX_NODES;  // [TILE_MAX_NODES + 4]
+  unsigned char* p = smem + (20 * TILE_MAX_NODES + 16);
+  // union: per-warp point records (facet phase) | staged halo points (domain phase of hex_tiled)
+  S.qp = p;
+  S.hnode = reinterpret_cast<int32_t*>(p);
+  S.hdat = reinterpret_cast<double*>(p + ((4 * (size_t)P.hmax + 15) / 16) * 16);
+  const size_t halo_bytes = P.hmax ? ((4 * (size_t)P.hmax + 15) / 16) * 16 + 8 * (size_t)P.hmax * P.hcomp : 0;
+  const size_t slot_bytes = (size_t)P.rec_bytes * warps;
+  p += ((halo_bytes > slot_bytes ? halo_bytes : slot_bytes) + 15) / 16 * 16;
+  S.vid = reinterpret_cast<int32_t*>(p);
+  p += 4 * (size_t)P.vmax;
+  S.vnode = reinterpret_cast<int32_t*>(p);
+  p += 4 * (size_t)P.vmax * NL;
+  S.vown = reinterpret_cast<int16_t*>(p);
+  p += 2 * (size_t)P.vmax * NL;
+  S.vhal = reinterpret_cast<int16_t*>(p);
+  p += P.hmax ? 2 * (size_t)P.vmax * NL : 0;
+  S.vfac = reinterpret_cast<int8_t*>(p);
+  p += P.vmax;
+  p = smem + (((size_t)(p - smem) + 15) / 16) * 16;
+  S.acc = reinterpret_cast<double*>(p);
+  S.H = 0;
+  return S;
+}
+
+// tile points, their row offsets (prefix of κ̂²·deg) and a zeroed accumulator
+template <int KH>
+__device__ __forceinline__ void tile_prologue(const TiledParams& P, TileSmem& S, int64_t tile) {
+  const int64_t n0 = P.tile_noff[tile];
+  const int T = (int)(P.tile_noff[tile + 1] - n0);
+  S.T = T;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int i = tid; i < T; i += nth) {
+    const int node = P.tile_node[n0 + i];
+    S.tnode[i] = node;
+    const int64_t rr = P.rowptr_s[node - P.own_lo];
+    S.trps[i] = rr;
+    S.tdeg[i] = (int)(P.rowptr_s[node - P.own_lo + 1] - rr);
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int carry = 0;
+    for (int base = 0; base < T; base += 32) {
+      const int i = base + tid;
+      int v = (i < T) ? KH * KH * S.tdeg[i] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (tid >= o) v += u;
+      }
+      if (i < T) S.toff[i + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (tid == 0) S.toff[0] = 0;
+  }
+  __syncthreads();
+  const int acc_n = P.values ? S.toff[T] : 0;
+  S.racc = S.acc + acc_n;
+  for (int i = tid; i < acc_n + KH * T; i += nth) S.acc[i] = 0.0;
+}
+
+// boundary terms: every facet visit of the tile, warp per visit, atomic accumulation
+template <int ET, int ORD, int KH, int Q>
+__device__ __forceinline__ void tile_facets(const TiledParams& P, const TileSmem& S, int64_t tile, unsigned char* slot) {
+  using C = TileCfg<ET, ORD, KH, Q>;
+  const int warp = threadIdx.x >> 5;
+  for (int f = 0; f < P.n_fac; f++) {
+    __syncthreads();
+    const int nv = load_visits<C::NL, true>(P, P.fvis[f], tile, S);
+    for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, true, false>(P, &P.fac[f], 1, S, v, slot);
+  }
+}
+
+// write every owned row once (coalesced, one warp per row) and the residual rows
+template <int KH>
+__device__ __forceinline__ void tile_epilogue(const TiledParams& P, const TileSmem& S) {
+  __syncthreads();
+  const int tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, T = S.T;
+  if (P.values) {
+    const int lane = tid & 31, nw = nth >> 5;
+    for (int rr = warp; rr < T * KH; rr += nw) {
+      const int li = rr / KH, k0 = rr % KH;
+      const int len = KH * S.tdeg[li];
+      const double* src = S.acc + S.toff[li] + k0 * len;
+      double* dst = P.values + (int64_t)k0 * KH * P.nnz_s + (int64_t)KH * S.trps[li];
+      for (int j = lane; j < len; j += 32) dst[j] = src[j];
+    }
+  }
+  if (P.rhs)
+    for (int t = tid; t < KH * T; t += nth) {
+      const int k0 = t / T, li = t % T;
+      P.rhs[(int64_t)k0 * P.n_own + (S.tnode[li] - P.own_lo)] = S.racc[t];
+    }
+}
+
+int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled);
+
+}  // namespace fem
