@@ -172,6 +172,12 @@ int fem_get_status(fem_mesh_t mesh, void* stream, int64_t* bad_elem);
 /* fem_mesh_info — host query: n_loc, kappa_hat, number of colours, number of node tiles. */
 int fem_mesh_info(fem_mesh_t mesh, int* n_loc, int* kappa_hat, int* n_colours, int64_t* n_tiles);
 
+/* fem_pattern_info — host query of the node-tile schedule built with the pattern:
+ * out[0] tiles, [1] largest tile (points), [2] largest accumulator (doubles), [3] largest packed record
+ * (bytes), [4] largest halo (points), [5] element visits in total, [6] largest per-tile visit count,
+ * [7] total packed record bytes. */
+int fem_pattern_info(fem_pattern_t pat, int64_t* out8);
+
 void fem_pattern_destroy(fem_pattern_t pat);
 void fem_mesh_destroy(fem_mesh_t mesh);
 const char* fem_last_error(void);

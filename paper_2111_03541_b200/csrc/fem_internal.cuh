@@ -57,7 +57,33 @@ struct TileSchedule {
   int64_t* halo_off = nullptr;   // device [n_tiles+1]: points of the elements a tile visits
   int32_t* halo_node = nullptr;  // device: sorted per tile
   int64_t max_halo = 0;
+  uint8_t* rec = nullptr;        // device: packed per-tile records (layout rec_layout)
+  int64_t* rec_off = nullptr;    // device [n_tiles+1] byte offsets
+  int64_t rec_max = 0, rec_bytes_total = 0;
 };
+
+// Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by
+// 16-byte aligned sections (see rec_layout).  Built on the host at pattern time (loc on the device).
+struct RecLayout {
+  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, size;
+};
+__host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, int nruns) {
+  RecLayout L;
+  int o = 32;
+  auto al = [](int x) { return (x + 15) & ~15; };
+  L.o_tnode = o; o = al(o + 4 * T);
+  L.o_tdeg = o;  o = al(o + 4 * T);
+  L.o_toff = o;  o = al(o + 4 * (T + 1));
+  L.o_trps = o;  o = al(o + 8 * T);
+  L.o_hnode = o; o = al(o + 4 * H);
+  L.o_run = o;   o = al(o + 4 * (nruns + 1));
+  L.o_velem = o; o = al(o + 4 * nv);
+  L.o_vhal = o;  o = al(o + 2 * nv * NL);
+  L.o_vown = o;  o = al(o + 2 * nv * NL);
+  L.o_vloc = o;  o = al(o + nv * NL * NL);
+  L.size = o;
+  return L;
+}
 
 }  // namespace fem
 

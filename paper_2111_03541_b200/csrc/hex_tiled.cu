@@ -14,6 +14,7 @@
 // (elements of one colour share no point), so the shared-memory accumulator takes plain adds and the
 // result is bit-identical run to run.  Boundary terms reuse the generic warp path (tiled.cuh).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "tiled.cuh"
@@ -51,11 +52,27 @@ struct HexCoef {  // combined coefficients of the batch's domain forms
   double kf0, Cf1; // Σ k f0, Σ C f1            (thermal matrix)
 };
 
+// What one visit needs: its ownership / halo indices / local column offsets, the staged halo data
+// and the tile accumulator (all in shared memory).
+struct HexView {
+  const int16_t* vown;   // [nv][8]
+  const uint16_t* vhal;  // [nv][8]
+  const int32_t* velem;  // [nv]
+  const uint8_t* vloc;   // [nv][64] (shared) or nullptr -> global P.loc
+  const double* hdat;    // [hcomp][H]
+  int H;
+  const int32_t* tdeg;
+  const int32_t* toff;
+  double* acc;
+  double* racc;
+  int T;
+};
+
 template <int KH, bool DET>
-__device__ __forceinline__ void hex_visit(const TiledParams& P, const TileSmem& S, const HexCoef& H, int v) {
+__device__ __forceinline__ void hex_visit(const TiledParams& P, const HexView& S, const HexCoef& H, int v) {
   const int lane = threadIdx.x & 31;
   const int16_t* own = S.vown + v * 8;
-  const int e = S.vid[v];
+  const int e = S.velem[v];
   // ---- stage G: Gauss point q = lane >> 2, nodes sub and sub + 4
   const int q = lane >> 2, sub = lane & 3;
   double J[3][3], Dr[KH][3], xq[3] = {0, 0, 0}, Tt = 0.0;
@@ -67,7 +84,7 @@ __device__ __forceinline__ void hex_visit(const TiledParams& P, const TileSmem& 
   for (int k = 0; k < KH; k++)
 #pragma unroll
     for (int j = 0; j < 3; j++) Dr[k][j] = 0.0;
-  const int16_t* hv = S.vhal + v * 8;
+  const uint16_t* hv = S.vhal + v * 8;
   const int HH = S.H;
 #pragma unroll
   for (int t = 0; t < 2; t++) {
@@ -249,7 +266,8 @@ __device__ __forceinline__ void hex_visit(const TiledParams& P, const TileSmem& 
 #pragma unroll
       for (int t = 0; t < 2; t++) {
         const int b = 2 * c + t;
-        double* rowb = base + __ldg(P.loc + (int64_t)e * 64 + a * 8 + b);
+        const int pos = S.vloc ? (int)S.vloc[v * 64 + a * 8 + b] : (int)__ldg(P.loc + (int64_t)e * 64 + a * 8 + b);
+        double* rowb = base + pos;
 #pragma unroll
         for (int i = 0; i < KH; i++)
 #pragma unroll
@@ -280,16 +298,18 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_tiled(const __grid_con
   __syncthreads();
   load_halo<3>(P, S, tile);
   const int nv = load_visits<8, false>(P, P.dvis, tile, S);
+  const HexView V{S.vown, reinterpret_cast<const uint16_t*>(S.vhal), S.vid, nullptr, S.hdat, S.H,
+                  S.tdeg, S.toff, S.acc, S.racc, S.T};
   if constexpr (DET) {
     const int64_t rb = P.dvis.roff[tile], re = P.dvis.roff[tile + 1];
     const int64_t vbase = P.dvis.run[rb];
     for (int64_t r = rb; r < re; r++) {  // colour runs: conflict-free, plain shared-memory adds
       const int v0 = (int)(P.dvis.run[r] - vbase), v1 = (int)(P.dvis.run[r + 1] - vbase);
-      for (int v = v0 + warp; v < v1; v += C::WARPS) hex_visit<KH, true>(P, S, H, v);
+      for (int v = v0 + warp; v < v1; v += C::WARPS) hex_visit<KH, true>(P, V, H, v);
       __syncthreads();
     }
   } else {  // warps flow freely; shared-memory fp64 atomics resolve the rare conflicts
-    for (int v = warp; v < nv; v += C::WARPS) hex_visit<KH, false>(P, S, H, v);
+    for (int v = warp; v < nv; v += C::WARPS) hex_visit<KH, false>(P, V, H, v);
   }
   unsigned char* slot = S.qp + (size_t)P.rec_bytes * warp;
   tile_facets<ET_HEX, 1, KH, 2>(P, S, tile, slot);
@@ -323,6 +343,161 @@ static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   return 0;
 }
 
+constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
+
+// ---- persistent record-driven kernel: one CTA per SM walks the tiles; the next tile's packed record
+// arrives by one TMA bulk copy and its halo points by LDGSTS while the current tile computes.
+__device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t* rec, double* hbuf) {
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+  const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
+  const RecLayout L = rec_layout(8, T, H, nv, nr);
+  const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
+  for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
+    const int c = t / H, i = t % H, node = hn[i];
+    const double* src = c < 3 ? P.coords + (int64_t)c * P.N + node : P.state + (int64_t)(c - 3) * P.N + node;
+    cp_async8(hbuf + t, src);
+  }
+  cp_async_commit();
+}
+
+template <int KH, bool DET>
+__global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_constant__ TiledParams P) {
+  using C = TileCfg<ET_HEX, 1, KH, 2>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  unsigned char* rbuf[2] = {smem + 128, smem + 128 + P.rec_cap};
+  double* hbuf[2];
+  hbuf[0] = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
+  hbuf[1] = hbuf[0] + P.hcap;
+  double* acc = hbuf[1] + P.hcap;
+  // facet-phase arrays (generic warp path)
+  TileSmem F;
+  unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
+  F.qp = fp;
+  fp += (size_t)P.rec_bytes * FACET_WARPS;
+  F.vid = reinterpret_cast<int32_t*>(fp);
+  fp += 4 * (size_t)P.fvmax;
+  F.vnode = reinterpret_cast<int32_t*>(fp);
+  fp += 4 * (size_t)P.fvmax * 8;
+  F.vown = reinterpret_cast<int16_t*>(fp);
+  fp += 2 * (size_t)P.fvmax * 8;
+  F.vfac = reinterpret_cast<int8_t*>(fp);
+  F.vhal = nullptr;
+  F.hnode = nullptr;
+  F.hdat = nullptr;
+  F.H = 0;
+  HexCoef Hc = {0, 0, 0, 0, 0, 0};
+  for (int f = 0; f < P.n_dom; f++) {
+    const FormArgs& Fm = P.dom[f];
+    Hc.cl += Fm.f0 * Fm.lam; Hc.cm += Fm.f0 * Fm.mu; Hc.sl += Fm.lam; Hc.sm += Fm.mu;
+    Hc.kf0 += Fm.p[1] * Fm.f0;
+    if (Fm.nu_hat >= 1) Hc.Cf1 += Fm.p[0] * Fm.f1;
+  }
+  const int tid = threadIdx.x, warp = tid >> 5;
+  int64_t tile = blockIdx.x;
+  if (tile >= P.n_tiles) return;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)(P.rec_off[tile + 1] - P.rec_off[tile]);
+    mbar_expect_tx(&mbar[0], bytes);
+    bulk_g2s(rbuf[0], P.rec + P.rec_off[tile], bytes, &mbar[0]);
+  }
+  mbar_wait(&mbar[0], 0);
+  gather_halo(P, rbuf[0], hbuf[0]);
+  for (int it = 0; tile < P.n_tiles; it++, tile += gridDim.x) {
+    const int cur = it & 1, oth = cur ^ 1;
+    const int64_t next = tile + gridDim.x;
+    if (tid == 0 && next < P.n_tiles) {  // prefetch the next record (its buffer was released last iteration)
+      const uint32_t bytes = (uint32_t)(P.rec_off[next + 1] - P.rec_off[next]);
+      mbar_expect_tx(&mbar[oth], bytes);
+      bulk_g2s(rbuf[oth], P.rec + P.rec_off[next], bytes, &mbar[oth]);
+    }
+    const uint8_t* rec = rbuf[cur];
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+    const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
+    const uint32_t fmask = (uint32_t)hdr[5];
+    const RecLayout L = rec_layout(8, T, H, nv, nr);
+    HexView V;
+    V.vown = reinterpret_cast<const int16_t*>(rec + L.o_vown);
+    V.vhal = reinterpret_cast<const uint16_t*>(rec + L.o_vhal);
+    V.velem = reinterpret_cast<const int32_t*>(rec + L.o_velem);
+    V.vloc = rec + L.o_vloc;
+    V.hdat = hbuf[cur];
+    V.H = H;
+    V.tdeg = reinterpret_cast<const int32_t*>(rec + L.o_tdeg);
+    V.toff = reinterpret_cast<const int32_t*>(rec + L.o_toff);
+    V.acc = acc;
+    V.racc = acc + acc_n;
+    V.T = T;
+    for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
+    cp_async_wait_all();
+    __syncthreads();
+    const int32_t* run = reinterpret_cast<const int32_t*>(rec + L.o_run);
+    if constexpr (DET) {
+      for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
+        for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS) hex_visit<KH, true>(P, V, Hc, v);
+        __syncthreads();
+      }
+    } else {
+      for (int v = warp; v < nv; v += C::WARPS) hex_visit<KH, false>(P, V, Hc, v);
+    }
+    if (next < P.n_tiles) {  // the next record has (almost surely) landed: start its halo gather
+      mbar_wait(&mbar[oth], (uint32_t)(((it + 1) >> 1) & 1));
+      gather_halo(P, rbuf[oth], hbuf[oth]);
+    }
+    // shared-memory view of the tile for the facet phase and the epilogue
+    F.tnode = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tnode));
+    F.tdeg = const_cast<int32_t*>(V.tdeg);
+    F.toff = const_cast<int32_t*>(V.toff);
+    F.trps = const_cast<int64_t*>(reinterpret_cast<const int64_t*>(rec + L.o_trps));
+    F.acc = acc;
+    F.racc = V.racc;
+    F.T = T;
+    if (fmask) tile_facets<ET_HEX, 1, KH, 2, FACET_WARPS>(P, F, tile, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
+    tile_epilogue<KH>(P, F);
+    __syncthreads();
+  }
+}
+
+template <int KH, bool DET>
+static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
+  using C = TileCfg<ET_HEX, 1, KH, 2>;
+  P.rec_bytes = (int)((sizeof(typename C::QPG) * C::NQF + 15) / 16 * 16);
+  int fv = 1;
+  for (int f = 0; f < P.n_fac; f++) fv = std::max<int>(fv, (int)P.fvis[f].max_per_tile);
+  P.fvmax = fv;
+  P.vmax = fv;
+  P.hmax = 0;
+  P.hcomp = 3 + KH * (P.nu_hat >= 1 ? 2 : 1);
+  P.rec = T.rec;
+  P.rec_off = T.rec_off;
+  P.n_tiles = T.n_tiles;
+  P.rec_cap = (int)((T.rec_max + 15) / 16 * 16);
+  P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
+  P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)KH * T.max_tile_nodes);
+  P.acc_cap = (P.acc_cap + 1) / 2 * 2;
+  const size_t fac_bytes = (size_t)P.rec_bytes * FACET_WARPS + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
+  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
+  if (smem > 227 * 1024) {
+    set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
+    return FEM_E_UNSUPPORTED;
+  }
+  FEM_CUDA_TRY(cudaFuncSetAttribute(k_hex_rec<KH, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (T.n_tiles <= 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
+  k_hex_rec<KH, DET><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 // Q1 hex, 2x2x2 points, domain terms all ELAST_DOMAIN (κ̂ = 3) or all THERMAL_DOMAIN (κ̂ = 1).
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled) {
   *handled = false;
@@ -333,6 +508,10 @@ int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cu
   }
   if (kh != 1 && kh != 3) return 0;
   *handled = true;
+  if (T.rec && !getenv("FEM_NO_RECORDS")) {
+    if (det) return kh == 3 ? run_hex_rec<3, true>(P, T, s) : run_hex_rec<1, true>(P, T, s);
+    return kh == 3 ? run_hex_rec<3, false>(P, T, s) : run_hex_rec<1, false>(P, T, s);
+  }
   if (det) return kh == 3 ? run_hex<3, true>(P, T, s) : run_hex<1, true>(P, T, s);
   return kh == 3 ? run_hex<3, false>(P, T, s) : run_hex<1, false>(P, T, s);
 }

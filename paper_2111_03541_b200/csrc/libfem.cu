@@ -260,6 +260,14 @@ int fem_pattern_build(fem_mesh_t m, void* stream, fem_pattern_t* out, int64_t* n
 
 int64_t fem_pattern_nnz_s(fem_pattern_t p) { return p ? p->nnz_s : -1; }
 
+int fem_pattern_info(fem_pattern_t p, int64_t* out) {
+  if (!p || !out) { set_error("fem_pattern_info: NULL argument"); return FEM_E_INVALID_ARG; }
+  const TileSchedule& T = p->tiles;
+  out[0] = T.n_tiles; out[1] = T.max_tile_nodes; out[2] = T.acc_max; out[3] = T.rec_max;
+  out[4] = T.max_halo; out[5] = T.visits_total; out[6] = T.dom.max_per_tile; out[7] = T.rec_bytes_total;
+  return 0;
+}
+
 int fem_pattern_export(fem_pattern_t p, int64_t* rowptr, int32_t* colidx, int32_t* slot_s, int64_t* rowptr_s,
                        int32_t* colidx_s, void* stream) {
   if (!p) { set_error("fem_pattern_export: NULL pattern"); return FEM_E_INVALID_ARG; }

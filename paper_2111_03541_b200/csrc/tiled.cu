@@ -27,13 +27,25 @@
 namespace fem {
 
 constexpr int64_t ACC_BUDGET_MAX = 16384;  // doubles (128 KB): hard cap of the row accumulator
-static int64_t acc_budget() {  // default 16384 doubles (128 KB): one 16-warp CTA per SM
-  static int64_t v = [] {
-    const char* s = getenv("FEM_TILE_ACC");
-    int64_t x = s ? atoll(s) : 16384;
-    return x < 256 ? 256 : (x > ACC_BUDGET_MAX ? ACC_BUDGET_MAX : x);
-  }();
-  return v;
+// Cap on element visits per tile (bounds the packed record, double-buffered in shared memory).
+static int64_t tile_visit_cap(int NL) {
+  const char* s = getenv("FEM_TILE_VISITS");
+  if (s) return atoll(s);
+  return NL == 8 ? 144 : (NL == 10 ? 320 : 768);
+}
+// Cap on halo points per tile (bounds the staged coordinates/state, double-buffered).
+static int64_t tile_halo_cap(int NL) {
+  const char* s = getenv("FEM_TILE_HALO");
+  if (s) return atoll(s);
+  return NL == 8 ? 300 : (NL == 10 ? 640 : 1024);
+}
+
+// Accumulator budget (doubles).  κ̂ = 1 rows are short, so a tile would hold hundreds of points and
+// its packed record (double-buffered in shared memory) would not fit: cap it at 4096 doubles.
+static int64_t acc_budget(int kh) {
+  const char* s = getenv("FEM_TILE_ACC");
+  int64_t x = s ? atoll(s) : (kh == 1 ? 4096 : 16384);
+  return x < 256 ? 256 : (x > ACC_BUDGET_MAX ? ACC_BUDGET_MAX : x);
 }
 
 // ------------------------------------------------------------------ host: tile schedule
@@ -76,6 +88,8 @@ static void free_visits(VisitList& V) {
 }
 
 void tiles_free(TileSchedule& T) {
+  cudaFree(T.rec);
+  cudaFree(T.rec_off);
   cudaFree(T.halo_off);
   cudaFree(T.halo_node);
   cudaFree(T.tile_noff);
@@ -89,7 +103,8 @@ void tiles_free(TileSchedule& T) {
 // Sort the visits of every tile by (colour, item) and cut colour runs.
 static int make_visits(int64_t n_tiles, const std::vector<int64_t>& voff, std::vector<int32_t>& items,
                        const std::vector<uint8_t>& colour_of_item, const int32_t* elem_of_item,
-                       const int8_t* facet_of_item, VisitList& V) {
+                       const int8_t* facet_of_item, VisitList& V, std::vector<int64_t>* roff_out = nullptr,
+                       std::vector<int64_t>* run_out = nullptr) {
   std::vector<int64_t> roff(n_tiles + 1, 0), run;
   run.reserve(items.size() / 8 + n_tiles + 1);
   for (int64_t t = 0; t < n_tiles; t++) {
@@ -120,7 +135,26 @@ static int make_visits(int64_t n_tiles, const std::vector<int64_t>& voff, std::v
     FEM_CUDA_TRY(cudaMalloc(&V.facet, sizeof(int8_t) * (fa.size() + 1)));
     if (!fa.empty()) FEM_CUDA_TRY(cudaMemcpy(V.facet, fa.data(), fa.size(), cudaMemcpyHostToDevice));
   }
+  if (roff_out) *roff_out = std::move(roff);
+  if (run_out) *run_out = std::move(run);
   return 0;
+}
+
+// Local column offsets of every (visit, a, b) written straight into the tile records.
+__global__ void k_fill_rec_loc(uint8_t* __restrict__ rec, const int64_t* __restrict__ vis_loc_off,
+                               const int32_t* __restrict__ vis_elem, int64_t n_vis, const int32_t* __restrict__ slot,
+                               const int32_t* __restrict__ conn, const int64_t* __restrict__ rowptr_s, int64_t E,
+                               int NL, int64_t lo, int64_t hi) {
+  const int64_t total = n_vis * NL * NL;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / (NL * NL);
+    const int ab = (int)(t % (NL * NL)), a = ab / NL;
+    const int64_t e = vis_elem[v];
+    const int64_t r = conn[(int64_t)a * E + e];
+    uint8_t val = 255;
+    if (r >= lo && r < hi) val = (uint8_t)(slot[(int64_t)ab * E + e] - rowptr_s[r - lo]);
+    rec[vis_loc_off[v] + ab] = val;
+  }
 }
 
 int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
@@ -139,7 +173,7 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     sz[i] = (int64_t)KH * KH * deg;
     max_sz = std::max(max_sz, sz[i]);
   }
-  const int64_t ACC_BUDGET = acc_budget();
+  const int64_t ACC_BUDGET = acc_budget(KH);
   if (max_sz > ACC_BUDGET) { set_error("tiled schedule: one row exceeds the shared accumulator"); return FEM_E_UNSUPPORTED; }
   // 1. Morton order of the owned points (spatial locality independent of the numbering)
   double bmin[3] = {1e300, 1e300, 1e300}, bmax[3] = {-1e300, -1e300, -1e300};
@@ -176,7 +210,27 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   std::vector<int64_t> tile_off{0};
   std::vector<int32_t> tile_nodes;
   tile_nodes.reserve(n_own);
-  int64_t cur_n = 0, cur_acc = 0, acc_max = 0;
+  // point -> element adjacency, to bound the number of element visits of a tile (its record size)
+  std::vector<int64_t> adj_off(n_own + 1, 0);
+  for (int64_t i = 0; i < (int64_t)NL * E; i++) {
+    const int64_t r = m->h_conn[i];
+    if (r >= lo && r < m->own_hi) adj_off[r - lo + 1]++;
+  }
+  for (int64_t i = 0; i < n_own; i++) adj_off[i + 1] += adj_off[i];
+  std::vector<int32_t> adj(adj_off[n_own]);
+  {
+    std::vector<int64_t> pos(adj_off.begin(), adj_off.end() - 1);
+    for (int64_t e = 0; e < E; e++)
+      for (int a = 0; a < NL; a++) {
+        const int64_t r = m->h_conn[(int64_t)a * E + e];
+        if (r >= lo && r < m->own_hi) adj[pos[r - lo]++] = (int32_t)e;
+      }
+  }
+  std::vector<int64_t> stamp(E, -1);  // element -> id of the last tile (or probe) that counted it
+  std::vector<int64_t> nstamp(N, -1); // point -> id of the last tile that counted it in its halo
+  int64_t stamp_id = 0;
+  const int64_t VISIT_CAP = tile_visit_cap(NL), HALO_CAP = tile_halo_cap(NL);
+  int64_t cur_n = 0, cur_acc = 0, cur_vis = 0, cur_halo = 0, acc_max = 0;
   int max_nodes = 0;
   auto close_tile = [&]() {
     if (cur_n == 0) return;
@@ -186,6 +240,41 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     max_nodes = std::max(max_nodes, (int)cur_n);
     cur_n = 0;
     cur_acc = 0;
+    cur_vis = 0;
+    cur_halo = 0;
+    stamp_id++;
+  };
+  // new elements a set of points would add to the current tile (without committing)
+  std::vector<int32_t> newe, newn;
+  int64_t probe_halo = 0;
+  auto probe = [&](int64_t g0, int64_t g1) {
+    newe.clear();
+    newn.clear();
+    for (int64_t i = g0; i < g1; i++) {
+      const int64_t li = key[i].second;
+      for (int64_t k = adj_off[li]; k < adj_off[li + 1]; k++)
+        if (stamp[adj[k]] != stamp_id) newe.push_back(adj[k]);
+    }
+    std::sort(newe.begin(), newe.end());
+    newe.erase(std::unique(newe.begin(), newe.end()), newe.end());
+    for (int32_t e : newe)
+      for (int a = 0; a < NL; a++) {
+        const int32_t r = m->h_conn[(int64_t)a * E + e];
+        if (nstamp[r] != stamp_id) newn.push_back(r);
+      }
+    std::sort(newn.begin(), newn.end());
+    newn.erase(std::unique(newn.begin(), newn.end()), newn.end());
+    probe_halo = (int64_t)newn.size();
+    return (int64_t)newe.size();
+  };
+  auto commit = [&](int64_t g0, int64_t g1, int64_t gacc) {
+    for (int64_t i = g0; i < g1; i++) tile_nodes.push_back((int32_t)(lo + key[i].second));
+    for (int32_t e : newe) stamp[e] = stamp_id;
+    for (int32_t r : newn) nstamp[r] = stamp_id;
+    cur_n += g1 - g0;
+    cur_acc += gacc;
+    cur_vis += (int64_t)newe.size();
+    cur_halo += probe_halo;
   };
   for (int64_t g0 = 0; g0 < n_own;) {
     int64_t g1 = g0 + 1;
@@ -193,18 +282,21 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     while (g1 < n_own && (key[g1].first >> (dim * L)) == gk) g1++;
     int64_t gacc = 0;
     for (int64_t i = g0; i < g1; i++) gacc += sz[key[i].second];
-    if (cur_n + (g1 - g0) <= TILE_MAX_NODES && cur_acc + gacc <= ACC_BUDGET) {
-      for (int64_t i = g0; i < g1; i++) tile_nodes.push_back((int32_t)(lo + key[i].second));
-      cur_n += g1 - g0;
-      cur_acc += gacc;
+    const int64_t gvis = probe(g0, g1);
+    if (cur_n + (g1 - g0) <= TILE_MAX_NODES && cur_acc + gacc <= ACC_BUDGET && cur_vis + gvis <= VISIT_CAP &&
+        cur_halo + probe_halo <= HALO_CAP) {
+      commit(g0, g1, gacc);
     } else {
       close_tile();
-      for (int64_t i = g0; i < g1; i++) {  // group alone: add node by node
+      for (int64_t i = g0; i < g1; i++) {  // group alone: add point by point
         const int64_t zi = sz[key[i].second];
-        if (cur_n + 1 > TILE_MAX_NODES || cur_acc + zi > ACC_BUDGET) close_tile();
-        tile_nodes.push_back((int32_t)(lo + key[i].second));
-        cur_n++;
-        cur_acc += zi;
+        int64_t vi = probe(i, i + 1);
+        if (cur_n + 1 > TILE_MAX_NODES || cur_acc + zi > ACC_BUDGET ||
+            (cur_n > 0 && (cur_vis + vi > VISIT_CAP || cur_halo + probe_halo > HALO_CAP))) {
+          close_tile();
+          vi = probe(i, i + 1);
+        }
+        commit(i, i + 1, zi);
       }
     }
     g0 = g1;
@@ -217,6 +309,9 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   std::vector<int32_t> tile_of(n_own);
   for (int64_t t = 0; t < n_tiles; t++)
     for (int64_t i = tile_off[t]; i < tile_off[t + 1]; i++) tile_of[tile_nodes[i] - lo] = (int32_t)t;
+  std::vector<int32_t> dom_items;
+  std::vector<int64_t> dom_cnt, dom_roff, dom_run;
+  std::vector<uint32_t> fac_mask(n_tiles, 0);
   // 3. element visits: (tile, element) for every distinct tile among the element's owned points
   auto tiles_of_elem = [&](int64_t e, int32_t* out) {
     int n = 0;
@@ -265,8 +360,13 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     FEM_CUDA_TRY(cudaMemcpy(T.halo_off, hoff.data(), sizeof(int64_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
     if (!hnode.empty())
       FEM_CUDA_TRY(cudaMemcpy(T.halo_node, hnode.data(), sizeof(int32_t) * hnode.size(), cudaMemcpyHostToDevice));
-    int rc = make_visits(n_tiles, cnt, items, m->h_colour, nullptr, nullptr, T.dom);
+    std::vector<int64_t> roff, run;
+    int rc = make_visits(n_tiles, cnt, items, m->h_colour, nullptr, nullptr, T.dom, &roff, &run);
     if (rc) return rc;
+    dom_items = std::move(items);
+    dom_cnt = std::move(cnt);
+    dom_roff = std::move(roff);
+    dom_run = std::move(run);
   }
   // 4. facet visits per boundary set
   T.bnd.resize(m->h_bset_elem.size());
@@ -287,6 +387,8 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     }
     int rc = make_visits(n_tiles, cnt, items, m->h_bset_colour[k], be.data(), m->h_bset_facet[k].data(), T.bnd[k]);
     if (rc) return rc;
+    for (int64_t t = 0; t < n_tiles; t++)
+      if (cnt[t + 1] > cnt[t] && k < 32) fac_mask[t] |= 1u << k;
   }
   // 5. device node lists + local column-offset table
   FEM_CUDA_TRY(cudaMalloc(&T.tile_noff, sizeof(int64_t) * (n_tiles + 1)));
@@ -301,6 +403,90 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     FEM_CUDA_TRY(cudaGetLastError());
   }
   FEM_CUDA_TRY(cudaStreamSynchronize(s));
+  // 6. packed per-tile records (one bulk copy per tile in the record-driven kernels)
+  {
+    std::vector<int64_t> roff(n_tiles + 1, 0);
+    std::vector<int32_t> halo;
+    std::vector<int64_t> hoff(n_tiles + 1, 0);
+    std::vector<int32_t> tmp;
+    for (int64_t t = 0; t < n_tiles; t++) {
+      const int64_t nvt = dom_cnt[t + 1] - dom_cnt[t];
+      tmp.clear();
+      for (int64_t i = dom_cnt[t]; i < dom_cnt[t + 1]; i++)
+        for (int a = 0; a < NL; a++) tmp.push_back(m->h_conn[(int64_t)a * E + dom_items[i]]);
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      halo.insert(halo.end(), tmp.begin(), tmp.end());
+      hoff[t + 1] = (int64_t)halo.size();
+      const int nruns = (int)(dom_roff[t + 1] - dom_roff[t]);
+      const RecLayout L = rec_layout(NL, (int)(tile_off[t + 1] - tile_off[t]), (int)tmp.size(), (int)nvt, nruns);
+      roff[t + 1] = roff[t] + L.size;
+      T.rec_max = std::max<int64_t>(T.rec_max, L.size);
+    }
+    std::vector<uint8_t> buf((size_t)roff[n_tiles], 0);
+    std::vector<int64_t> vis_loc(dom_items.size());
+    for (int64_t t = 0; t < n_tiles; t++) {
+      const int Tn = (int)(tile_off[t + 1] - tile_off[t]);
+      const int H = (int)(hoff[t + 1] - hoff[t]);
+      const int nv = (int)(dom_cnt[t + 1] - dom_cnt[t]);
+      const int nruns = (int)(dom_roff[t + 1] - dom_roff[t]);
+      const RecLayout L = rec_layout(NL, Tn, H, nv, nruns);
+      uint8_t* r = buf.data() + roff[t];
+      int32_t* hdr = reinterpret_cast<int32_t*>(r);
+      const int32_t* tn = tile_nodes.data() + tile_off[t];
+      const int32_t* hn = halo.data() + hoff[t];
+      int32_t* o_tnode = reinterpret_cast<int32_t*>(r + L.o_tnode);
+      int32_t* o_tdeg = reinterpret_cast<int32_t*>(r + L.o_tdeg);
+      int32_t* o_toff = reinterpret_cast<int32_t*>(r + L.o_toff);
+      int64_t* o_trps = reinterpret_cast<int64_t*>(r + L.o_trps);
+      int acc = 0;
+      o_toff[0] = 0;
+      for (int i = 0; i < Tn; i++) {
+        const int64_t li = tn[i] - lo;
+        o_tnode[i] = tn[i];
+        o_trps[i] = rps[li];
+        o_tdeg[i] = (int32_t)(rps[li + 1] - rps[li]);
+        acc += KH * KH * o_tdeg[i];
+        o_toff[i + 1] = acc;
+      }
+      hdr[0] = Tn; hdr[1] = H; hdr[2] = nv; hdr[3] = nruns; hdr[4] = acc; hdr[5] = (int32_t)fac_mask[t];
+      memcpy(r + L.o_hnode, hn, sizeof(int32_t) * H);
+      int32_t* o_run = reinterpret_cast<int32_t*>(r + L.o_run);
+      for (int k = 0; k <= nruns; k++) o_run[k] = (int32_t)(dom_run[dom_roff[t] + k] - dom_cnt[t]);
+      int32_t* o_velem = reinterpret_cast<int32_t*>(r + L.o_velem);
+      uint16_t* o_vhal = reinterpret_cast<uint16_t*>(r + L.o_vhal);
+      int16_t* o_vown = reinterpret_cast<int16_t*>(r + L.o_vown);
+      for (int v = 0; v < nv; v++) {
+        const int64_t gi = dom_cnt[t] + v;
+        const int32_t e = dom_items[gi];
+        o_velem[v] = e;
+        for (int a = 0; a < NL; a++) {
+          const int32_t node = m->h_conn[(int64_t)a * E + e];
+          o_vhal[v * NL + a] = (uint16_t)(std::lower_bound(hn, hn + H, node) - hn);
+          const int32_t* f = std::lower_bound(tn, tn + Tn, node);
+          o_vown[v * NL + a] = (f != tn + Tn && *f == node) ? (int16_t)(f - tn) : (int16_t)-1;
+        }
+        vis_loc[gi] = roff[t] + L.o_vloc + (int64_t)v * NL * NL;
+      }
+    }
+    FEM_CUDA_TRY(cudaMalloc(&T.rec, buf.size() + 16));
+    FEM_CUDA_TRY(cudaMalloc(&T.rec_off, sizeof(int64_t) * (n_tiles + 1)));
+    FEM_CUDA_TRY(cudaMemcpy(T.rec, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+    FEM_CUDA_TRY(cudaMemcpy(T.rec_off, roff.data(), sizeof(int64_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
+    T.rec_bytes_total = (int64_t)buf.size();
+    int64_t* d_vloc = nullptr;
+    FEM_CUDA_TRY(cudaMalloc(&d_vloc, sizeof(int64_t) * (vis_loc.size() + 1)));
+    FEM_CUDA_TRY(cudaMemcpy(d_vloc, vis_loc.data(), sizeof(int64_t) * vis_loc.size(), cudaMemcpyHostToDevice));
+    const int64_t tot = (int64_t)vis_loc.size() * NL * NL;
+    if (tot > 0) {
+      const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 32);
+      k_fill_rec_loc<<<(unsigned)blocks, 256, 0, s>>>(T.rec, d_vloc, T.dom.elem, (int64_t)vis_loc.size(), p->slot,
+                                                       m->conn, p->rowptr_s, E, NL, lo, m->own_hi);
+      FEM_CUDA_TRY(cudaGetLastError());
+    }
+    FEM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(d_vloc);
+  }
   return 0;
 }
 

@@ -38,6 +38,14 @@ struct TiledParams {
   const int32_t* halo_node;
   int hmax;      // capacity of the halo arrays (0: halo staging off)
   int hcomp;     // doubles per halo point: dim coords + κ̂·(ν̂+1) state values
+  // record-driven (persistent) kernels
+  const uint8_t* rec;
+  const int64_t* rec_off;
+  int64_t n_tiles;
+  int rec_cap;   // bytes of one record buffer
+  int hcap;      // doubles of one halo buffer
+  int acc_cap;   // doubles of the accumulator (incl. residual rows)
+  int fvmax;     // capacity of the facet visit arrays
 };
 
 // Lean point record for elasticity-only domain visits: w, ∇N_a, and w·σ.
@@ -488,14 +496,15 @@ __device__ __forceinline__ void tile_prologue(const TiledParams& P, TileSmem& S,
 }
 
 // boundary terms: every facet visit of the tile, warp per visit, atomic accumulation
-template <int ET, int ORD, int KH, int Q>
+template <int ET, int ORD, int KH, int Q, int NW = TILED_THREADS / 32>
 __device__ __forceinline__ void tile_facets(const TiledParams& P, const TileSmem& S, int64_t tile, unsigned char* slot) {
   using C = TileCfg<ET, ORD, KH, Q>;
   const int warp = threadIdx.x >> 5;
   for (int f = 0; f < P.n_fac; f++) {
     __syncthreads();
     const int nv = load_visits<C::NL, true>(P, P.fvis[f], tile, S);
-    for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, true, false>(P, &P.fac[f], 1, S, v, slot);
+    if (warp < NW)
+      for (int v = warp; v < nv; v += NW) warp_visit<ET, ORD, KH, Q, true, false>(P, &P.fac[f], 1, S, v, slot);
   }
 }
 
@@ -520,6 +529,33 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const TileSm
       P.rhs[(int64_t)k0 * P.n_own + (S.tnode[li] - P.own_lo)] = S.racc[t];
     }
 }
+
+// ---- async copy helpers: TMA bulk copies (cp.async.bulk + mbarrier) and LDGSTS gathers (cp.async)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled);
 

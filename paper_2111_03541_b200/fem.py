@@ -114,6 +114,7 @@ def lib():
         L.fem_pattern_nnz_s.argtypes = [V]
         L.fem_pattern_nnz_s.restype = I64
         L.fem_pattern_export.argtypes = [V, V, V, V, V, V, V]
+        L.fem_pattern_info.argtypes = [V, V]
         L.fem_assemble_matrix.argtypes = [V, V, PP, V, V, I, I, V]
         L.fem_assemble_residual.argtypes = [V, V, PP, V, V, I, I, V]
         L.fem_assemble_system.argtypes = [V, V, PP, V, V, V, I, I, V]
@@ -131,7 +132,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pattern_export",
+EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pattern_export", "fem_pattern_info",
             "fem_assemble_matrix", "fem_assemble_residual", "fem_assemble_system", "fem_residual_norms",
             "fem_linearize_host", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version"]
@@ -196,6 +197,14 @@ def fem_pattern_build(mesh_h, stream=None):
 
 def fem_pattern_nnz_s(pat_h):
     return lib().fem_pattern_nnz_s(pat_h)
+
+
+def fem_pattern_info(pat_h):
+    out = np.zeros(8, dtype=np.int64)
+    _check(lib().fem_pattern_info(pat_h, out.ctypes.data))
+    keys = ["tiles", "max_tile_points", "max_acc_doubles", "max_record_bytes", "max_halo_points", "visits",
+            "max_tile_visits", "record_bytes"]
+    return dict(zip(keys, out.tolist()))
 
 
 def fem_pattern_export(pat_h, rowptr=None, colidx=None, slot_s=None, rowptr_s=None, colidx_s=None, stream=None):

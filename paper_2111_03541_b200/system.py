@@ -35,7 +35,10 @@ class FemSystem:
         self.rhs = None
 
     def info(self):
-        return fem.fem_mesh_info(self.mesh_h)
+        d = fem.fem_mesh_info(self.mesh_h)
+        if self.pat_h:
+            d.update(fem.fem_pattern_info(self.pat_h))
+        return d
 
     def alloc(self, matrix=True, residual=True):
         if matrix and self.values is None:
