@@ -15,6 +15,7 @@
 // result is bit-identical run to run.  Boundary terms reuse the generic warp path (tiled.cuh).
 #include <algorithm>
 #include <cstdlib>
+#include <cuda/std/utility>
 #include <string>
 
 #include "tiled.cuh"
@@ -344,6 +345,172 @@ static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
 }
 
 constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
+constexpr int HEX_SCRATCH = 160; // doubles of per-warp scratch of hex_visit_el (aliases the facet slots)
+
+// Reference-gradient B fragments of the geometry GEMM (constant per lane): for k-step s and n-tile t,
+// lane l holds ∇̂N_a(ξ_q)_j with a = 4s + (l&3), (q, j) = divmod(8t + (l>>2), 3).
+struct GeoFrag {
+  double b[2][3];
+};
+__device__ __forceinline__ GeoFrag geo_frag() {
+  GeoFrag F;
+  const int l = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < 2; s++)
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      const int a = 4 * s + (l & 3), n = 8 * t + (l >> 2), q = n / 3, j = n % 3;
+      double g[3], N;
+      hex_ref(a, q, g, N);
+      F.b[s][t] = g[j];
+    }
+  return F;
+}
+
+// Lean elasticity visit (κ̂ = 3).  Geometry as one GEMM on the fp64 tensor cores:
+//   [J(q) | ∇̂d(q)]_{r,(q,j)} = Σ_a [x_a; d_a]_r ∇̂N_a(ξ_q)_j   (6 x 8) · (8 x 24)  = 6 DMMA,
+// then per point (lanes q = l>>2): J^{-1}, w = det J, ∇d = ∇̂d J^{-1}, S = w σ; the per-point records
+// go through a per-warp shared scratch to the fragment layout (a = l>>2, points c, c+4) for the Gram
+// tiles (18 DMMA) and the residual rows.
+template <bool DET>
+__device__ __forceinline__ void hex_visit_el(const TiledParams& P, const HexView& S, const HexCoef& H,
+                                             const GeoFrag& GF, double* sc, int v) {
+  const int lane = threadIdx.x & 31;
+  const int16_t* own = S.vown + v * 8;
+  const uint16_t* hv = S.vhal + v * 8;
+  const int HH = S.H;
+  const int c = lane & 3, r = lane >> 2;
+  // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
+  double C3[3][2];
+#pragma unroll
+  for (int t = 0; t < 3; t++) { C3[t][0] = 0.0; C3[t][1] = 0.0; }
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const double av = r < 6 ? S.hdat[r * HH + hv[4 * s + c]] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; t++) dmma884(C3[t], av, GF.b[s][t]);
+  }
+  if (r < 6) {
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      sc[r * 24 + 8 * t + 2 * c] = C3[t][0];
+      sc[r * 24 + 8 * t + 2 * c + 1] = C3[t][1];
+    }
+  }
+  __syncwarp();
+  // ---- per point q = lane >> 2 (4 lanes per point compute the same values)
+  const int q = r;
+  double J[3][3], Dr[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      J[i][j] = sc[i * 24 + 3 * q + j];
+      Dr[i][j] = sc[(3 + i) * 24 + 3 * q + j];
+    }
+  const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+  if (__any_sync(0xffffffffu, !(det > 0.0))) {
+    if (lane == 0) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)S.velem[v]);
+    return;
+  }
+  const double rr = 1.0 / det;
+  double Ji[3][3];
+  Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+  double gu[3][3];
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+#pragma unroll
+    for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+  __syncwarp();  // everyone has read the GEMM output; the scratch now takes the per-point records
+  if (c == 0) {
+    double* o = sc + q * 20;
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+      for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
+    o[9] = det;  // w (unit Gauss-Legendre weights)
+    const double lw = H.sl * det * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * det;
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+  }
+  __syncwarp();
+  // ---- fragment layout: node a = lane >> 2, points c and c + 4
+  const int a = r;
+  const double* o0 = sc + c * 20;
+  const double* o1 = sc + (c + 4) * 20;
+  double g0[3], g1[3], N0, N1, G0[3], G1[3];
+  hex_ref(a, c, g0, N0);
+  hex_ref(a, c + 4, g1, N1);
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    G0[i] = o0[0 * 3 + i] * g0[0] + o0[1 * 3 + i] * g0[1] + o0[2 * 3 + i] * g0[2];
+    G1[i] = o1[0 * 3 + i] * g1[0] + o1[1 * 3 + i] * g1[1] + o1[2 * 3 + i] * g1[2];
+  }
+  const double w0 = o0[9], w1 = o1[9];
+  const int li = own[a];
+  if (P.rhs) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
+    double res[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        t = fma(o0[10 + i * 3 + j], G0[j], t);
+        t = fma(o1[10 + i * 3 + j], G1[j], t);
+      }
+      res[i] = -sum4(t);
+    }
+    if (c == 0 && li >= 0) {
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        if constexpr (DET) S.racc[i * S.T + li] += res[i];
+        else atomicAdd(S.racc + i * S.T + li, res[i]);
+      }
+    }
+  }
+  if (P.values) {
+    double M[3][3][2];
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        M[j][k][0] = 0.0;
+        M[j][k][1] = 0.0;
+        dmma884(M[j][k], w0 * G0[j], G0[k]);
+        dmma884(M[j][k], w1 * G1[j], G1[k]);
+      }
+    if (li >= 0) {
+      const int d = S.tdeg[li];
+      double* base = S.acc + S.toff[li];
+      const uint8_t* lc = S.vloc + v * 64 + a * 8 + 2 * c;
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+        double* rowb = base + lc[t];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) {
+            const double kv = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+            if constexpr (DET) rowb[(i * 3 + m) * d] += kv;
+            else atomicAdd(rowb + (i * 3 + m) * d, kv);
+          }
+      }
+    }
+  }
+  __syncwarp();  // scratch is reused by the next visit
+}
 
 // ---- persistent record-driven kernel: one CTA per SM walks the tiles; the next tile's packed record
 // arrives by one TMA bulk copy and its halo points by LDGSTS while the current tile computes.
@@ -374,7 +541,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
   TileSmem F;
   unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
   F.qp = fp;
-  fp += (size_t)P.rec_bytes * FACET_WARPS;
+  fp += std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS);
   F.vid = reinterpret_cast<int32_t*>(fp);
   fp += 4 * (size_t)P.fvmax;
   F.vnode = reinterpret_cast<int32_t*>(fp);
@@ -394,6 +561,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     if (Fm.nu_hat >= 1) Hc.Cf1 += Fm.p[0] * Fm.f1;
   }
   const int tid = threadIdx.x, warp = tid >> 5;
+  const GeoFrag GF = geo_frag();
   int64_t tile = blockIdx.x;
   if (tile >= P.n_tiles) return;
   if (tid == 0) {
@@ -438,13 +606,20 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     cp_async_wait_all();
     __syncthreads();
     const int32_t* run = reinterpret_cast<const int32_t*>(rec + L.o_run);
+    double* wsc = reinterpret_cast<double*>(F.qp) + (size_t)HEX_SCRATCH * warp;
     if constexpr (DET) {
       for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
-        for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS) hex_visit<KH, true>(P, V, Hc, v);
+        for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS) {
+          if constexpr (KH == 3) hex_visit_el<true>(P, V, Hc, GF, wsc, v);
+          else hex_visit<KH, true>(P, V, Hc, v);
+        }
         __syncthreads();
       }
     } else {
-      for (int v = warp; v < nv; v += C::WARPS) hex_visit<KH, false>(P, V, Hc, v);
+      for (int v = warp; v < nv; v += C::WARPS) {
+        if constexpr (KH == 3) hex_visit_el<false>(P, V, Hc, GF, wsc, v);
+        else hex_visit<KH, false>(P, V, Hc, v);
+      }
     }
     if (next < P.n_tiles) {  // the next record has (almost surely) landed: start its halo gather
       mbar_wait(&mbar[oth], (uint32_t)(((it + 1) >> 1) & 1));
@@ -481,7 +656,7 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
   P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)KH * T.max_tile_nodes);
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
-  const size_t fac_bytes = (size_t)P.rec_bytes * FACET_WARPS + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
+  const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
   const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
   if (smem > 227 * 1024) {
     set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
