@@ -31,20 +31,21 @@ constexpr int64_t ACC_BUDGET_MAX = 16384;  // doubles (128 KB): hard cap of the 
 static int64_t tile_visit_cap(int NL) {
   const char* s = getenv("FEM_TILE_VISITS");
   if (s) return atoll(s);
-  return NL == 8 ? 144 : (NL == 10 ? 320 : 768);
+  return NL == 8 ? 144 : (NL == 10 ? 240 : 640);
 }
 // Cap on halo points per tile (bounds the staged coordinates/state, double-buffered).
 static int64_t tile_halo_cap(int NL) {
   const char* s = getenv("FEM_TILE_HALO");
   if (s) return atoll(s);
-  return NL == 8 ? 300 : (NL == 10 ? 640 : 1024);
+  return NL == 8 ? 300 : (NL == 10 ? 480 : 640);
 }
 
 // Accumulator budget (doubles).  κ̂ = 1 rows are short, so a tile would hold hundreds of points and
 // its packed record (double-buffered in shared memory) would not fit: cap it at 4096 doubles.
-static int64_t acc_budget(int kh) {
+static int64_t acc_budget(int kh, int nl) {
   const char* s = getenv("FEM_TILE_ACC");
   int64_t x = s ? atoll(s) : (kh == 1 ? 4096 : 16384);
+  (void)nl;
   return x < 256 ? 256 : (x > ACC_BUDGET_MAX ? ACC_BUDGET_MAX : x);
 }
 
@@ -173,7 +174,7 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     sz[i] = (int64_t)KH * KH * deg;
     max_sz = std::max(max_sz, sz[i]);
   }
-  const int64_t ACC_BUDGET = acc_budget(KH);
+  const int64_t ACC_BUDGET = acc_budget(KH, NL);
   if (max_sz > ACC_BUDGET) { set_error("tiled schedule: one row exceeds the shared accumulator"); return FEM_E_UNSUPPORTED; }
   // 1. Morton order of the owned points (spatial locality independent of the numbering)
   double bmin[3] = {1e300, 1e300, 1e300}, bmax[3] = {-1e300, -1e300, -1e300};
@@ -511,9 +512,155 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_tiled(const __grid_constan
   tile_epilogue<KH>(P, S);
 }
 
+// ---- persistent record-driven generic kernel (tets, triangles, hex with other forms): the next tile's
+// packed record arrives by one TMA bulk copy while the current tile computes; the tile's halo points
+// (coordinates + state) are staged in shared memory once per tile; warps take element visits freely
+// and accumulate with shared-memory fp64 atomics.
+template <int NL, int DIM>
+__device__ __forceinline__ void gather_halo_gen(const TiledParams& P, const uint8_t* rec, double* hbuf) {
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+  const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
+  const RecLayout L = rec_layout(NL, T, H, nv, nr);
+  const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
+  for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
+    const int c = t / H, i = t % H, node = hn[i];
+    const double* src = c < DIM ? P.coords + (int64_t)c * P.N + node : P.state + (int64_t)(c - DIM) * P.N + node;
+    cp_async8(hbuf + t, src);
+  }
+  cp_async_commit();
+}
+
+template <int ET, int ORD, int KH, int Q>
+__global__ void __launch_bounds__(TILED_THREADS, 1) k_gen_rec(const __grid_constant__ TiledParams P) {
+  using C = TileCfg<ET, ORD, KH, Q>;
+  constexpr int NL = C::NL, DIM = C::DIM;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  unsigned char* rbuf[2] = {smem + 128, smem + 128 + P.rec_cap};
+  double* hbuf = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
+  double* acc = hbuf + P.hcap;
+  TileSmem S;
+  unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
+  S.qp = fp;
+  fp += (size_t)P.rec_bytes * C::WARPS;
+  S.vid = reinterpret_cast<int32_t*>(fp);  // facet-phase visit arrays
+  fp += 4 * (size_t)P.fvmax;
+  S.vnode = reinterpret_cast<int32_t*>(fp);
+  fp += 4 * (size_t)P.fvmax * NL;
+  S.vown = reinterpret_cast<int16_t*>(fp);
+  fp += 2 * (size_t)P.fvmax * NL;
+  S.vfac = reinterpret_cast<int8_t*>(fp);
+  S.vhal = nullptr;
+  S.hnode = nullptr;
+  S.hdat = nullptr;
+  S.H = 0;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  unsigned char* slot = S.qp + (size_t)P.rec_bytes * warp;
+  int64_t tile = blockIdx.x;
+  if (tile >= P.n_tiles) return;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)(P.rec_off[tile + 1] - P.rec_off[tile]);
+    mbar_expect_tx(&mbar[0], bytes);
+    bulk_g2s(rbuf[0], P.rec + P.rec_off[tile], bytes, &mbar[0]);
+  }
+  for (int it = 0; tile < P.n_tiles; it++, tile += gridDim.x) {
+    const int cur = it & 1, oth = cur ^ 1;
+    const int64_t next = tile + gridDim.x;
+    mbar_wait(&mbar[cur], (uint32_t)((it >> 1) & 1));
+    if (tid == 0 && next < P.n_tiles) {  // prefetch the next record
+      const uint32_t bytes = (uint32_t)(P.rec_off[next + 1] - P.rec_off[next]);
+      mbar_expect_tx(&mbar[oth], bytes);
+      bulk_g2s(rbuf[oth], P.rec + P.rec_off[next], bytes, &mbar[oth]);
+    }
+    const uint8_t* rec = rbuf[cur];
+    gather_halo_gen<NL, DIM>(P, rec, hbuf);
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+    const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
+    const uint32_t fmask = (uint32_t)hdr[5];
+    const RecLayout L = rec_layout(NL, T, H, nv, nr);
+    TileSmem D = S;  // domain view: everything from the record + the staged halo
+    D.tnode = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tnode));
+    D.tdeg = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tdeg));
+    D.toff = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_toff));
+    D.trps = const_cast<int64_t*>(reinterpret_cast<const int64_t*>(rec + L.o_trps));
+    D.vid = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_velem));
+    D.vown = const_cast<int16_t*>(reinterpret_cast<const int16_t*>(rec + L.o_vown));
+    D.vhal = const_cast<int16_t*>(reinterpret_cast<const int16_t*>(rec + L.o_vhal));
+    D.vloc = rec + L.o_vloc;
+    D.hdat = hbuf;
+    D.H = H;
+    D.acc = acc;
+    D.racc = acc + acc_n;
+    D.T = T;
+    for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
+    cp_async_wait_all();
+    __syncthreads();
+    if (P.lean)
+      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, D, v, slot);
+    else
+      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, D, v, slot);
+    TileSmem F = D;  // facet phase: global visit lists, global point data
+    F.vid = S.vid;
+    F.vnode = S.vnode;
+    F.vown = S.vown;
+    F.vfac = S.vfac;
+    F.vhal = nullptr;
+    F.vloc = nullptr;
+    F.hdat = nullptr;
+    F.H = 0;
+    if (fmask) tile_facets<ET, ORD, KH, Q>(P, F, tile, slot);
+    tile_epilogue<KH>(P, F);
+    __syncthreads();
+  }
+}
+
+template <int ET, int ORD, int KH, int Q>
+static int run_gen_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
+  using C = TileCfg<ET, ORD, KH, Q>;
+  constexpr int NL = C::NL, DIM = C::DIM;
+  const size_t rec_dom = (P.lean ? sizeof(typename C::QPL) : sizeof(typename C::QPG)) * C::NQV;
+  const size_t rec_fac = sizeof(typename C::QPG) * C::NQF;
+  P.rec_bytes = (int)((std::max(rec_dom, rec_fac) + 15) / 16 * 16);
+  int fv = 1;
+  for (int f = 0; f < P.n_fac; f++) fv = std::max<int>(fv, (int)P.fvis[f].max_per_tile);
+  P.fvmax = fv;
+  P.vmax = fv;
+  P.hmax = 0;
+  P.hcomp = DIM + KH * (P.nu_hat >= 1 ? 2 : 1);
+  P.rec = T.rec;
+  P.rec_off = T.rec_off;
+  P.n_tiles = T.n_tiles;
+  P.rec_cap = (int)((T.rec_max + 15) / 16 * 16);
+  P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
+  P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)KH * T.max_tile_nodes);
+  P.acc_cap = (P.acc_cap + 1) / 2 * 2;
+  const size_t fac_bytes = (size_t)P.rec_bytes * C::WARPS + (size_t)fv * (4 + NL * 6 + 1) + 16;
+  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
+  if (smem > 227 * 1024) {
+    set_error("record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
+    return FEM_E_UNSUPPORTED;
+  }
+  FEM_CUDA_TRY(cudaFuncSetAttribute(k_gen_rec<ET, ORD, KH, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (T.n_tiles <= 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
+  k_gen_rec<ET, ORD, KH, Q><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 template <int ET, int ORD, int KH, int Q>
 static int run_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   using C = TileCfg<ET, ORD, KH, Q>;
+  if (T.rec && getenv("FEM_GEN_RECORDS")) return run_gen_rec<ET, ORD, KH, Q>(P, T, s);
   constexpr int NL = C::NL;
   const size_t rec_dom = (P.lean ? sizeof(typename C::QPL) : sizeof(typename C::QPG)) * C::NQV;
   const size_t rec_fac = sizeof(typename C::QPG) * C::NQF;

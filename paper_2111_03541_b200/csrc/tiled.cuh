@@ -101,6 +101,7 @@ struct TileSmem {
   int16_t* vown;   // [vmax*NL] tile-local point index or -1
   unsigned char* qp;  // per-warp point-record slots
   int16_t* vhal;   // [vmax*NL] halo index of each visit point
+  const uint8_t* vloc = nullptr;  // [vmax][NL][NL] local column offsets in shared memory (records)
   int32_t* hnode;  // [hmax]
   double* hdat;    // [hcomp][hmax] staged coordinates and state of the halo points
   int H;
@@ -144,7 +145,8 @@ __device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs*
     if (a % NSUB == sub) {
       double X[DIM];
 #pragma unroll
-      for (int d = 0; d < DIM; d++) X[d] = __ldg(P.coords + (int64_t)d * P.N + nd[a]);
+      for (int d = 0; d < DIM; d++)
+        X[d] = S.hdat ? S.hdat[d * S.H + (uint16_t)S.vhal[v * NL + a]] : __ldg(P.coords + (int64_t)d * P.N + nd[a]);
 #pragma unroll
       for (int i = 0; i < DIM; i++) {
         xp[i] = fma(N[a], X[i], xp[i]);
@@ -237,9 +239,12 @@ __device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs*
       }
 #pragma unroll
       for (int k = 0; k < KH; k++) {
-        const double s0 = __ldg(P.state + (int64_t)k * P.N + nd[a]);
+        const int hi = S.hdat ? (uint16_t)S.vhal[v * NL + a] : 0;
+        const double s0 = S.hdat ? S.hdat[(DIM + k) * S.H + hi] : __ldg(P.state + (int64_t)k * P.N + nd[a]);
         u0[k] = fma(N[a], s0, u0[k]);
-        if (!LEAN && P.nu_hat >= 1) u1[k] = fma(N[a], __ldg(P.state + ((int64_t)KH + k) * P.N + nd[a]), u1[k]);
+        if (!LEAN && P.nu_hat >= 1)
+          u1[k] = fma(N[a], S.hdat ? S.hdat[(DIM + KH + k) * S.H + hi] : __ldg(P.state + ((int64_t)KH + k) * P.N + nd[a]),
+                      u1[k]);
 #pragma unroll
         for (int d = 0; d < DIM; d++) gu[k][d] = fma(Ga[d], s0, gu[k][d]);
       }
@@ -321,7 +326,7 @@ __device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs*
     const int li = own[a];
     if (is_mat) {
       const int b = t % NL;
-      const int pos = __ldg(P.loc + (int64_t)e * (NL * NL) + a * NL + b);
+      const int pos = S.vloc ? (int)S.vloc[v * (NL * NL) + a * NL + b] : (int)__ldg(P.loc + (int64_t)e * (NL * NL) + a * NL + b);
       double K[KH][KH];
 #pragma unroll
       for (int i = 0; i < KH; i++)
@@ -439,7 +444,7 @@ __device__ __forceinline__ TileSmem tile_smem_layout(unsigned char* smem, const 
   // union: per-warp point records (facet phase) | staged halo points (domain phase of hex_tiled)
   S.qp = p;
   S.hnode = reinterpret_cast<int32_t*>(p);
-  S.hdat = reinterpret_cast<double*>(p + ((4 * (size_t)P.hmax + 15) / 16) * 16);
+  S.hdat = P.hmax ? reinterpret_cast<double*>(p + ((4 * (size_t)P.hmax + 15) / 16) * 16) : nullptr;
   const size_t halo_bytes = P.hmax ? ((4 * (size_t)P.hmax + 15) / 16) * 16 + 8 * (size_t)P.hmax * P.hcomp : 0;
   const size_t slot_bytes = (size_t)P.rec_bytes * warps;
   p += ((halo_bytes > slot_bytes ? halo_bytes : slot_bytes) + 15) / 16 * 16;
