@@ -65,9 +65,11 @@ struct TileSchedule {
 // Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by
 // 16-byte aligned sections (see rec_layout).  Built on the host at pattern time (loc on the device).
 struct RecLayout {
-  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, size;
+  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, o_fcnt, o_fdv, o_ffac, size;
 };
-__host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, int nruns) {
+// header[6] = number of boundary sets nb, header[7] = facet visits nf; facet visit i of set k
+// (fcnt[k] <= i < fcnt[k+1]) is facet ffac[i] of the tile's domain visit fdv[i].
+__host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, int nruns, int nb = 0, int nf = 0) {
   RecLayout L;
   int o = 32;
   auto al = [](int x) { return (x + 15) & ~15; };
@@ -81,8 +83,14 @@ __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, in
   L.o_vhal = o;  o = al(o + 2 * nv * NL);
   L.o_vown = o;  o = al(o + 2 * nv * NL);
   L.o_vloc = o;  o = al(o + nv * NL * NL);
+  L.o_fcnt = o;  o = al(o + 4 * (nb + 1));
+  L.o_fdv = o;   o = al(o + 2 * nf);
+  L.o_ffac = o;  o = al(o + nf);
   L.size = o;
   return L;
+}
+__host__ __device__ inline RecLayout rec_layout_hdr(int NL, const int32_t* h) {
+  return rec_layout(NL, h[0], h[1], h[2], h[3], h[6], h[7]);
 }
 
 }  // namespace fem

@@ -517,7 +517,7 @@ __device__ __forceinline__ void hex_visit_el(const TiledParams& P, const HexView
 __device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t* rec, double* hbuf) {
   const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
   const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
-  const RecLayout L = rec_layout(8, T, H, nv, nr);
+  const RecLayout L = rec_layout_hdr(8, hdr);
   const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
   for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
     const int c = t / H, i = t % H, node = hn[i];
@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
   using C = TileCfg<ET_HEX, 1, KH, 2>;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  int* ctr = reinterpret_cast<int*>(smem + 64);
   unsigned char* rbuf[2] = {smem + 128, smem + 128 + P.rec_cap};
   double* hbuf[2];
   hbuf[0] = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
@@ -589,7 +590,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
     const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
     const uint32_t fmask = (uint32_t)hdr[5];
-    const RecLayout L = rec_layout(8, T, H, nv, nr);
+    const RecLayout L = rec_layout_hdr(8, hdr);
     HexView V;
     V.vown = reinterpret_cast<const int16_t*>(rec + L.o_vown);
     V.vhal = reinterpret_cast<const uint16_t*>(rec + L.o_vhal);
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     V.acc = acc;
     V.racc = acc + acc_n;
     V.T = T;
+    if (tid == 0) *ctr = 0;
     for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
     cp_async_wait_all();
     __syncthreads();
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
         __syncthreads();
       }
     } else {
-      for (int v = warp; v < nv; v += C::WARPS) {
+      for (int v = warp; v < nv; v += C::WARPS) {  // hex visits are uniform: static split
         if constexpr (KH == 3) hex_visit_el<false>(P, V, Hc, GF, wsc, v);
         else hex_visit<KH, false>(P, V, Hc, v);
       }
@@ -633,7 +635,13 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     F.acc = acc;
     F.racc = V.racc;
     F.T = T;
-    if (fmask) tile_facets<ET_HEX, 1, KH, 2, FACET_WARPS>(P, F, tile, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
+    F.vid = const_cast<int32_t*>(V.velem);
+    F.vown = const_cast<int16_t*>(V.vown);
+    F.vhal = const_cast<int16_t*>(reinterpret_cast<const int16_t*>(V.vhal));
+    F.vloc = V.vloc;
+    F.hdat = const_cast<double*>(V.hdat);
+    F.H = H;
+    if (fmask) rec_facets<ET_HEX, 1, KH, 2, FACET_WARPS>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
     tile_epilogue<KH>(P, F);
     __syncthreads();
   }

@@ -1,0 +1,306 @@
+// tet1_ns.cu — the c4 hot path: SUPG/PSPG-stabilised Navier-Stokes (code P:1002-1022) on
+// P1/P1 tetrahedra with the 4-point degree-2 rule, node-tile owner gather (tiled.cu records).
+//
+// P1 tets are affine: J, det J, ∇N_a and every operand gradient (∇u_k, ∇p, Rc = u_k,k) are constant
+// over the element; only the values N_a(γ) = α or β (barycentric 4-point rule) and u(γ) vary, and
+// Rm_i(γ) = ρ u_k(γ) u_i,k + p_,i is linear in u(γ) (u_i,kk = 0, reading L10).  A warp takes two
+// element visits at once: lane (h, a, b) with h = lane>>4 computes the geometry of visit h and the
+// 4x4 block of the pair (a, b) summed over the 4 points; the same lanes then take the residual rows
+// (a, κ0).  Contributions go to the tile accumulator with shared-memory fp64 atomics.  Boundary
+// groups (inflow/outflow/fix) reuse the generic warp path.
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "tiled.cuh"
+
+namespace fem {
+
+struct NsCoef {
+  double rho, mu, tm, tc, f0;
+};
+
+// Per-visit point data in the warp scratch (doubles): G[4][3] | gu[4][3] | Rc | w | u[4 points][4] | Rm[4][3]
+constexpr int NS_SC = 12 + 12 + 2 + 16 + 12;  // 54 doubles per visit
+
+__device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& D, const NsCoef& c, int v0, int nv,
+                                          double* scw) {
+  const int lane = threadIdx.x & 31;
+  const int h = lane >> 4, l16 = lane & 15;
+  const int v = v0 + h;
+  const bool valid = v < nv;
+  const int vv = valid ? v : v0;
+  const double al = 0.13819660112501051518, be = 0.58541019662496845446;  // (5-√5)/20, (5+3√5)/20
+  double* sc = scw + h * NS_SC;
+  // ---- phase 1: lane 0 of each half-warp computes the visit's constants (affine P1 tet)
+  bool bad = false;
+  if (l16 == 0) {
+    double X[4][3], U[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; n++) {
+      const int hh = (uint16_t)D.vhal[vv * 4 + n];
+#pragma unroll
+      for (int d = 0; d < 3; d++) X[n][d] = D.hdat[d * D.H + hh];
+#pragma unroll
+      for (int k = 0; k < 4; k++) U[k][n] = D.hdat[(3 + k) * D.H + hh];
+    }
+    double J[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) J[i][j] = X[j + 1][i] - X[0][i];
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    bad = valid && !(det > 0.0);
+    const double rr = 1.0 / det;
+    double Ji[3][3];
+    Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+    double G[4][3];  // ∇N_0 = -(row sums of J^{-1}), ∇N_k = row k-1 of J^{-1}
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      G[1][i] = Ji[0][i];
+      G[2][i] = Ji[1][i];
+      G[3][i] = Ji[2][i];
+      G[0][i] = -(Ji[0][i] + Ji[1][i] + Ji[2][i]);
+    }
+#pragma unroll
+    for (int n = 0; n < 4; n++)
+#pragma unroll
+      for (int i = 0; i < 3; i++) sc[n * 3 + i] = G[n][i];
+    double gu[4][3];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        gu[k][i] = U[k][0] * G[0][i] + U[k][1] * G[1][i] + U[k][2] * G[2][i] + U[k][3] * G[3][i];
+        sc[12 + k * 3 + i] = gu[k][i];
+      }
+    sc[24] = gu[0][0] + gu[1][1] + gu[2][2];  // Rc
+    sc[25] = det * (1.0 / 24.0);                // w (4-point rule weight 1/24)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      double u[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        u[k] = al * (U[k][0] + U[k][1] + U[k][2] + U[k][3]) + (be - al) * U[k][q];
+        sc[26 + q * 4 + k] = u[k];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; i++)  // Rm_i = ρ u_k u_i,k + p_,i
+        sc[42 + q * 3 + i] = gu[3][i] + c.rho * (u[0] * gu[i][0] + u[1] * gu[i][1] + u[2] * gu[i][2]);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (bad) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)D.vid[v]);
+    __syncwarp();
+    return;
+  }
+  __syncwarp();
+  // ---- phase 2: lane (a, b): the 4x4 block of the pair and the residual row (a, κ0 = b)
+  const double rho = c.rho, mu = c.mu, tm = c.tm, tc = c.tc;
+  const int a = l16 >> 2, b = l16 & 3;
+  const int li = D.vown[vv * 4 + a];
+  double Ga[3], Gb[3];
+#pragma unroll
+  for (int i = 0; i < 3; i++) { Ga[i] = sc[a * 3 + i]; Gb[i] = sc[b * 3 + i]; }
+  const double w = sc[25], Rc = sc[24];
+  double GaGb = 0.0, smv[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) GaGb = fma(Ga[k], Gb[k], GaGb);
+#pragma unroll
+  for (int m = 0; m < 3; m++) smv[m] = Ga[0] * sc[12 + 0 * 3 + m] + Ga[1] * sc[12 + 1 * 3 + m] + Ga[2] * sc[12 + 2 * 3 + m];
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int m = 0; m < 4; m++) acc[i][m] = 0.0;
+  double res = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const double* u = sc + 26 + q * 4;
+    const double* Rm = sc + 42 + q * 3;
+    const double Na = (a == q) ? be : al, Nb = (b == q) ? be : al;
+    const double Aa = Ga[0] * u[0] + Ga[1] * u[1] + Ga[2] * u[2];
+    const double Bb = Gb[0] * u[0] + Gb[1] * u[1] + Gb[2] * u[2];
+    const double wNb = w * Nb;
+    const double diag = w * (-rho * Nb * Aa + mu * GaGb + tm * rho * rho * Aa * Bb);
+    const double c_uu = w * tm * rho * rho * Aa * Nb;
+    const double c_rm = tm * rho * wNb;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const double ui = u[i], Rmi = Rm[i];
+#pragma unroll
+      for (int m = 0; m < 3; m++) {
+        double t = Ga[m] * (c_rm * Rmi - rho * wNb * ui) + c_uu * sc[12 + i * 3 + m] + tc * w * Ga[i] * Gb[m];
+        if (i == m) t += diag;
+        acc[i][m] += t;
+      }
+      acc[i][3] += w * (-Ga[i] * Nb + tm * rho * Aa * Gb[i]);
+      acc[3][i] += w * (Na * Gb[i] + tm * rho * (Nb * smv[i] + Ga[i] * Bb));
+    }
+    acc[3][3] += w * tm * GaGb;
+    if (b < 3) {  // residual row (a, u_b): BASE + SUPG of NS_domain
+      const int i = b;
+      double r = -Ga[i] * u[3] + tc * Ga[i] * Rc + tm * rho * Aa * Rm[i];
+#pragma unroll
+      for (int j = 0; j < 3; j++) r += Ga[j] * (mu * sc[12 + i * 3 + j] - rho * u[i] * u[j]);
+      res += w * r;
+    } else {       // residual row (a, p)
+      res += w * (Na * Rc + tm * (Ga[0] * Rm[0] + Ga[1] * Rm[1] + Ga[2] * Rm[2]));
+    }
+  }
+  if (valid && li >= 0) {
+    if (P.values) {
+      const int d = D.tdeg[li];
+      double* rowb = D.acc + D.toff[li] + D.vloc[vv * 16 + a * 4 + b];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int m = 0; m < 4; m++) atomicAdd(rowb + (i * 4 + m) * d, c.f0 * acc[i][m]);
+    }
+    if (P.rhs) atomicAdd(D.racc + b * D.T + li, res);
+  }
+  __syncwarp();  // scratch reused by the next pair of visits
+}
+
+template <bool PAD>
+__global__ void __launch_bounds__(TILED_THREADS, 1) k_ns_rec(const __grid_constant__ TiledParams P) {
+  using C = TileCfg<ET_TET, 1, 4, 2>;
+  constexpr int NL = 4, DIM = 3;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  int* ctr = reinterpret_cast<int*>(smem + 64);
+  unsigned char* rbuf[2] = {smem + 128, smem + 128 + P.rec_cap};
+  double* hbuf = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
+  double* acc = hbuf + P.hcap;
+  TileSmem S;
+  unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
+  S.qp = fp;
+  fp += std::max((size_t)P.rec_bytes * 8, (size_t)8 * 2 * NS_SC * C::WARPS);
+  S.vid = reinterpret_cast<int32_t*>(fp);
+  fp += 4 * (size_t)P.fvmax;
+  S.vnode = reinterpret_cast<int32_t*>(fp);
+  fp += 4 * (size_t)P.fvmax * NL;
+  S.vown = reinterpret_cast<int16_t*>(fp);
+  fp += 2 * (size_t)P.fvmax * NL;
+  S.vfac = reinterpret_cast<int8_t*>(fp);
+  S.vhal = nullptr;
+  S.hnode = nullptr;
+  S.hdat = nullptr;
+  S.H = 0;
+  NsCoef cf;
+  cf.rho = P.dom[0].p[0]; cf.mu = P.dom[0].p[1]; cf.tm = P.dom[0].p[2]; cf.tc = P.dom[0].p[3]; cf.f0 = P.dom[0].f0;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  unsigned char* slot = S.qp + (size_t)P.rec_bytes * (warp % 8);
+  int64_t tile = blockIdx.x;
+  if (tile >= P.n_tiles) return;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = (uint32_t)(P.rec_off[tile + 1] - P.rec_off[tile]);
+    mbar_expect_tx(&mbar[0], bytes);
+    bulk_g2s(rbuf[0], P.rec + P.rec_off[tile], bytes, &mbar[0]);
+  }
+  for (int it = 0; tile < P.n_tiles; it++, tile += gridDim.x) {
+    const int cur = it & 1, oth = cur ^ 1;
+    const int64_t next = tile + gridDim.x;
+    mbar_wait(&mbar[cur], (uint32_t)((it >> 1) & 1));
+    if (tid == 0 && next < P.n_tiles) {
+      const uint32_t bytes = (uint32_t)(P.rec_off[next + 1] - P.rec_off[next]);
+      mbar_expect_tx(&mbar[oth], bytes);
+      bulk_g2s(rbuf[oth], P.rec + P.rec_off[next], bytes, &mbar[oth]);
+    }
+    const uint8_t* rec = rbuf[cur];
+    {  // stage the tile's halo points
+      const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+      const RecLayout L = rec_layout_hdr(NL, hdr);
+      const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
+      const int H = hdr[1];
+      for (int t = tid; t < H * P.hcomp; t += blockDim.x) {
+        const int cc = t / H, i = t % H, node = hn[i];
+        const double* src = cc < DIM ? P.coords + (int64_t)cc * P.N + node : P.state + (int64_t)(cc - DIM) * P.N + node;
+        cp_async8(hbuf + t, src);
+      }
+      cp_async_commit();
+    }
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+    const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
+    const uint32_t fmask = (uint32_t)hdr[5];
+    const RecLayout L = rec_layout_hdr(NL, hdr);
+    TileSmem D = S;
+    D.tnode = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tnode));
+    D.tdeg = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tdeg));
+    D.toff = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_toff));
+    D.trps = const_cast<int64_t*>(reinterpret_cast<const int64_t*>(rec + L.o_trps));
+    D.vid = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_velem));
+    D.vown = const_cast<int16_t*>(reinterpret_cast<const int16_t*>(rec + L.o_vown));
+    D.vhal = const_cast<int16_t*>(reinterpret_cast<const int16_t*>(rec + L.o_vhal));
+    D.vloc = rec + L.o_vloc;
+    D.hdat = hbuf;
+    D.H = H;
+    D.acc = acc;
+    D.racc = acc + acc_n;
+    D.T = T;
+    for (int i = tid; i < acc_n + 4 * T; i += blockDim.x) acc[i] = 0.0;
+    if (tid == 0) *ctr = 0;
+    cp_async_wait_all();
+    __syncthreads();
+    double* scw = reinterpret_cast<double*>(S.qp) + (size_t)2 * NS_SC * warp;
+    for (int v0 = grab_visits(ctr, 2); v0 < nv; v0 = grab_visits(ctr, 2)) ns_visit2(P, D, cf, v0, nv, scw);
+    if (fmask) rec_facets<ET_TET, 1, 4, 2, 8>(P, D, rec, L, slot);
+    tile_epilogue<4>(P, D);
+    __syncthreads();
+  }
+}
+
+// NS on P1 tets, 4-point rule, exactly one domain term NS_DOMAIN.
+int launch_ns_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled) {
+  *handled = false;
+  if (P.n_dom != 1 || P.dom[0].form != FEM_WF_NS_DOMAIN || !T.rec) return 0;
+  *handled = true;
+  using C = TileCfg<ET_TET, 1, 4, 2>;
+  constexpr int NL = 4;
+  P.rec_bytes = (int)((sizeof(typename C::QPG) * C::NQF + 15) / 16 * 16);
+  int fv = 1;
+  for (int f = 0; f < P.n_fac; f++) fv = std::max<int>(fv, (int)P.fvis[f].max_per_tile);
+  P.fvmax = fv;
+  P.vmax = fv;
+  P.hmax = 0;
+  P.hcomp = 3 + 4;
+  P.rec = T.rec;
+  P.rec_off = T.rec_off;
+  P.n_tiles = T.n_tiles;
+  P.rec_cap = (int)((T.rec_max + 15) / 16 * 16);
+  P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
+  P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)4 * T.max_tile_nodes);
+  P.acc_cap = (P.acc_cap + 1) / 2 * 2;
+  const size_t fac_bytes = std::max((size_t)P.rec_bytes * 8, (size_t)8 * 2 * NS_SC * C::WARPS) + (size_t)fv * (4 + NL * 6 + 1) + 16;
+  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
+  if (smem > 227 * 1024) {
+    set_error("NS record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
+    return FEM_E_UNSUPPORTED;
+  }
+  FEM_CUDA_TRY(cudaFuncSetAttribute(k_ns_rec<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (T.n_tiles <= 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
+  k_ns_rec<false><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace fem

@@ -313,6 +313,8 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   std::vector<int32_t> dom_items;
   std::vector<int64_t> dom_cnt, dom_roff, dom_run;
   std::vector<uint32_t> fac_mask(n_tiles, 0);
+  std::vector<std::vector<int64_t>> fac_cnt;   // per boundary set: facet-visit offsets per tile
+  std::vector<std::vector<int32_t>> fac_items; // per boundary set: facet entries, tile-major
   // 3. element visits: (tile, element) for every distinct tile among the element's owned points
   auto tiles_of_elem = [&](int64_t e, int32_t* out) {
     int n = 0;
@@ -390,6 +392,8 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     if (rc) return rc;
     for (int64_t t = 0; t < n_tiles; t++)
       if (cnt[t + 1] > cnt[t] && k < 32) fac_mask[t] |= 1u << k;
+    fac_cnt.push_back(std::move(cnt));
+    fac_items.push_back(std::move(items));
   }
   // 5. device node lists + local column-offset table
   FEM_CUDA_TRY(cudaMalloc(&T.tile_noff, sizeof(int64_t) * (n_tiles + 1)));
@@ -420,7 +424,10 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
       halo.insert(halo.end(), tmp.begin(), tmp.end());
       hoff[t + 1] = (int64_t)halo.size();
       const int nruns = (int)(dom_roff[t + 1] - dom_roff[t]);
-      const RecLayout L = rec_layout(NL, (int)(tile_off[t + 1] - tile_off[t]), (int)tmp.size(), (int)nvt, nruns);
+      int nf = 0;
+      for (size_t k = 0; k < fac_cnt.size(); k++) nf += (int)(fac_cnt[k][t + 1] - fac_cnt[k][t]);
+      const RecLayout L = rec_layout(NL, (int)(tile_off[t + 1] - tile_off[t]), (int)tmp.size(), (int)nvt, nruns,
+                                     (int)fac_cnt.size(), nf);
       roff[t + 1] = roff[t] + L.size;
       T.rec_max = std::max<int64_t>(T.rec_max, L.size);
     }
@@ -431,7 +438,10 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
       const int H = (int)(hoff[t + 1] - hoff[t]);
       const int nv = (int)(dom_cnt[t + 1] - dom_cnt[t]);
       const int nruns = (int)(dom_roff[t + 1] - dom_roff[t]);
-      const RecLayout L = rec_layout(NL, Tn, H, nv, nruns);
+      const int nb = (int)fac_cnt.size();
+      int nf = 0;
+      for (int k = 0; k < nb; k++) nf += (int)(fac_cnt[k][t + 1] - fac_cnt[k][t]);
+      const RecLayout L = rec_layout(NL, Tn, H, nv, nruns, nb, nf);
       uint8_t* r = buf.data() + roff[t];
       int32_t* hdr = reinterpret_cast<int32_t*>(r);
       const int32_t* tn = tile_nodes.data() + tile_off[t];
@@ -451,6 +461,27 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
         o_toff[i + 1] = acc;
       }
       hdr[0] = Tn; hdr[1] = H; hdr[2] = nv; hdr[3] = nruns; hdr[4] = acc; hdr[5] = (int32_t)fac_mask[t];
+      hdr[6] = nb; hdr[7] = nf;
+      {  // facet visits: (domain visit of the facet's element, facet id)
+        std::vector<std::pair<int32_t, int16_t>> ev(nv);
+        for (int v = 0; v < nv; v++) ev[v] = {dom_items[dom_cnt[t] + v], (int16_t)v};
+        std::sort(ev.begin(), ev.end());
+        int32_t* o_fcnt = reinterpret_cast<int32_t*>(r + L.o_fcnt);
+        int16_t* o_fdv = reinterpret_cast<int16_t*>(r + L.o_fdv);
+        int8_t* o_ffac = reinterpret_cast<int8_t*>(r + L.o_ffac);
+        int i = 0;
+        for (int k = 0; k < nb; k++) {
+          o_fcnt[k] = i;
+          for (int64_t j = fac_cnt[k][t]; j < fac_cnt[k][t + 1]; j++, i++) {
+            const int32_t entry = fac_items[k][j];
+            const int32_t e = m->h_bset_elem[k][entry];
+            auto f = std::lower_bound(ev.begin(), ev.end(), std::make_pair(e, (int16_t)-32768));
+            o_fdv[i] = f->second;
+            o_ffac[i] = m->h_bset_facet[k][entry];
+          }
+        }
+        o_fcnt[nb] = i;
+      }
       memcpy(r + L.o_hnode, hn, sizeof(int32_t) * H);
       int32_t* o_run = reinterpret_cast<int32_t*>(r + L.o_run);
       for (int k = 0; k <= nruns; k++) o_run[k] = (int32_t)(dom_run[dom_roff[t] + k] - dom_cnt[t]);
@@ -520,7 +551,7 @@ template <int NL, int DIM>
 __device__ __forceinline__ void gather_halo_gen(const TiledParams& P, const uint8_t* rec, double* hbuf) {
   const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
   const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
-  const RecLayout L = rec_layout(NL, T, H, nv, nr);
+  const RecLayout L = rec_layout_hdr(NL, hdr);
   const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
   for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
     const int c = t / H, i = t % H, node = hn[i];
@@ -536,6 +567,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_gen_rec(const __grid_const
   constexpr int NL = C::NL, DIM = C::DIM;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  int* ctr = reinterpret_cast<int*>(smem + 64);
   unsigned char* rbuf[2] = {smem + 128, smem + 128 + P.rec_cap};
   double* hbuf = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
   double* acc = hbuf + P.hcap;
@@ -583,7 +615,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_gen_rec(const __grid_const
     const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
     const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
     const uint32_t fmask = (uint32_t)hdr[5];
-    const RecLayout L = rec_layout(NL, T, H, nv, nr);
+    const RecLayout L = rec_layout_hdr(NL, hdr);
     TileSmem D = S;  // domain view: everything from the record + the staged halo
     D.tnode = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tnode));
     D.tdeg = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tdeg));
@@ -599,23 +631,17 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_gen_rec(const __grid_const
     D.racc = acc + acc_n;
     D.T = T;
     for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
+    if (tid == 0) *ctr = 0;
     cp_async_wait_all();
     __syncthreads();
     if (P.lean)
-      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, D, v, slot);
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1))
+        warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, D, v, slot);
     else
-      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, D, v, slot);
-    TileSmem F = D;  // facet phase: global visit lists, global point data
-    F.vid = S.vid;
-    F.vnode = S.vnode;
-    F.vown = S.vown;
-    F.vfac = S.vfac;
-    F.vhal = nullptr;
-    F.vloc = nullptr;
-    F.hdat = nullptr;
-    F.H = 0;
-    if (fmask) tile_facets<ET, ORD, KH, Q>(P, F, tile, slot);
-    tile_epilogue<KH>(P, F);
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1))
+        warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, D, v, slot);
+    if (fmask) rec_facets<ET, ORD, KH, Q, C::WARPS>(P, D, rec, L, slot);
+    tile_epilogue<KH>(P, D);
     __syncthreads();
   }
 }
@@ -709,6 +735,7 @@ int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_proble
     } else {
       if (P.n_fac == MAX_FAC_TERMS) { set_error("tiled: too many boundary terms"); return FEM_E_UNSUPPORTED; }
       P.fvis[P.n_fac] = T.bnd[term.region];
+      P.fac_set[P.n_fac] = term.region;
       P.fac[P.n_fac++] = make_form_args(prob, term);
     }
   }
@@ -726,6 +753,11 @@ int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_proble
   if (et == ET_HEX && o == 1 && q == 2 && !getenv("FEM_NO_HEX_MMA")) {
     bool handled = false;
     const int rc = launch_hex_tiled(P, T, kh, getenv("FEM_TILED_DET") != nullptr, s, &handled);
+    if (handled) return rc;
+  }
+  if (et == ET_TET && o == 1 && kh == 4 && q == 2 && !getenv("FEM_NO_NS_SPEC")) {
+    bool handled = false;
+    const int rc = launch_ns_tiled(P, T, s, &handled);
     if (handled) return rc;
   }
   if (et == ET_TRI && o == 1) {

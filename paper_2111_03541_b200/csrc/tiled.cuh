@@ -32,6 +32,7 @@ struct TiledParams {
   double* rhs;
   long long* err;
   int nu_hat;
+  int fac_set[MAX_FAC_TERMS];  // boundary set of each facet term
   int vmax;      // capacity of the per-tile visit arrays
   int rec_bytes; // bytes of one warp's point-record slot
   const int64_t* halo_off;  // per tile: sorted points of the visited elements
@@ -113,7 +114,7 @@ struct TileSmem {
 // One warp assembles one element (or facet) visit into the tile accumulator.
 template <int ET, int ORD, int KH, int Q, bool FACET, bool LEAN>
 __device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs* forms, int nforms, const TileSmem& S,
-                                           int v, unsigned char* slot) {
+                                           int v, unsigned char* slot, int fac_override = -1) {
   using C = TileCfg<ET, ORD, KH, Q>;
   using EL = typename C::EL;
   constexpr int DIM = C::DIM, NL = C::NL;
@@ -129,7 +130,7 @@ __device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs*
   const bool gl = g < NQ;
   const int gq = gl ? g : 0;
   double xi[3] = {0, 0, 0}, wref, mref[3] = {0, 0, 0};
-  if constexpr (FACET) EL::fac_qp(Q, S.vfac[v], gq, xi, wref, mref);
+  if constexpr (FACET) EL::fac_qp(Q, fac_override >= 0 ? fac_override : S.vfac[v], gq, xi, wref, mref);
   else EL::vol_qp(Q, gq, xi, wref);
   double N[NL], dN[NL][DIM];
   EL::shape(xi, N, dN);
@@ -513,6 +514,31 @@ __device__ __forceinline__ void tile_facets(const TiledParams& P, const TileSmem
   }
 }
 
+// Dynamic work distribution inside a tile: a warp grabs `step` visits from a shared counter.
+__device__ __forceinline__ int grab_visits(int* ctr, int step) {
+  int v = 0;
+  if ((threadIdx.x & 31) == 0) v = atomicAdd(ctr, step);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// Boundary terms from the tile record: facet visit i of set k is facet ffac[i] of domain visit fdv[i]
+// (the domain view D carries the staged halo and the local column offsets).
+template <int ET, int ORD, int KH, int Q, int NW>
+__device__ __forceinline__ void rec_facets(const TiledParams& P, const TileSmem& D, const uint8_t* rec,
+                                           const RecLayout& L, unsigned char* slot) {
+  const int32_t* fcnt = reinterpret_cast<const int32_t*>(rec + L.o_fcnt);
+  const int16_t* fdv = reinterpret_cast<const int16_t*>(rec + L.o_fdv);
+  const int8_t* ffac = reinterpret_cast<const int8_t*>(rec + L.o_ffac);
+  const int warp = threadIdx.x >> 5;
+  __syncthreads();  // per-warp slots may alias scratch used by the domain phase
+  if (warp >= NW) return;
+  for (int f = 0; f < P.n_fac; f++) {
+    const int k = P.fac_set[f];
+    for (int i = fcnt[k] + warp; i < fcnt[k + 1]; i += NW)
+      warp_visit<ET, ORD, KH, Q, true, false>(P, &P.fac[f], 1, D, fdv[i], slot, ffac[i]);
+  }
+}
+
 // write every owned row once (coalesced, one warp per row) and the residual rows
 template <int KH>
 __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const TileSmem& S) {
@@ -563,5 +589,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled);
+int launch_ns_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled);
 
 }  // namespace fem
