@@ -345,7 +345,7 @@ static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
 }
 
 constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
-constexpr int HEX_SCRATCH = 160; // doubles of per-warp scratch of hex_visit_el (aliases the facet slots)
+constexpr int HEX_SCRATCH = 160; // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
 
 // Reference-gradient B fragments of the geometry GEMM (constant per lane): for k-step s and n-tile t,
 // lane l holds ∇̂N_a(ξ_q)_j with a = 4s + (l&3), (q, j) = divmod(8t + (l>>2), 3).
@@ -527,17 +527,171 @@ __device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t*
   cp_async_commit();
 }
 
+// Offsets (bytes from the dynamic shared-memory base) of the current tile's arrays: kept in shared
+// memory so every visit addresses them with LDS and without rematerialising the record layout.
+struct TileOffs {
+  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc;
+  int H, T;
+};
+// Per-lane constants of the fragment layout: B fragments of the geometry GEMM (6), ∇̂N_a at points c
+// and c+4 (6), N_a at c and c+4 (2); lane l = 4a + c.
+constexpr int LANE_TAB = 14;
+
+template <bool DET>
+__device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOffs& to, const HexCoef& H,
+                                              const double* __restrict__ lt, double* sc, int v,
+                                              unsigned char* sm) {
+  const int lane = threadIdx.x & 31;
+  const int16_t* own = reinterpret_cast<const int16_t*>(sm + to.vown) + v * 8;
+  const uint16_t* hv = reinterpret_cast<const uint16_t*>(sm + to.vhal) + v * 8;
+  const double* hdat = reinterpret_cast<const double*>(sm + to.hdat);
+  const int HH = to.H;
+  const int c = lane & 3, r = lane >> 2;
+  const double* L = lt + lane * LANE_TAB;
+  // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
+  double C3[3][2];
+#pragma unroll
+  for (int t = 0; t < 3; t++) { C3[t][0] = 0.0; C3[t][1] = 0.0; }
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    const double av = r < 6 ? hdat[r * HH + hv[4 * s + c]] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; t++) dmma884(C3[t], av, L[s * 3 + t]);
+  }
+  if (r < 6) {
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+      sc[r * 24 + 8 * t + 2 * c] = C3[t][0];
+      sc[r * 24 + 8 * t + 2 * c + 1] = C3[t][1];
+    }
+  }
+  __syncwarp();
+  const int q = r;
+  double J[3][3], Dr[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      J[i][j] = sc[i * 24 + 3 * q + j];
+      Dr[i][j] = sc[(3 + i) * 24 + 3 * q + j];
+    }
+  const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+  if (__any_sync(0xffffffffu, !(det > 0.0))) {
+    if (lane == 0)
+      atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL),
+                (unsigned long long)reinterpret_cast<const int32_t*>(sm + to.velem)[v]);
+    __syncwarp();
+    return;
+  }
+  __syncwarp();  // everyone has read the GEMM output; the scratch now takes the per-point records
+  if (c == 0) {
+    const double rr = 1.0 / det;
+    double Ji[3][3];
+    Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+    double gu[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+#pragma unroll
+      for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+    double* o = sc + q * 20;  // per-point records (the GEMM output has been consumed)
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+      for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
+    o[9] = det;  // w (unit Gauss-Legendre weights)
+    const double lw = H.sl * det * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * det;
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+  }
+  __syncwarp();
+  // ---- fragment layout: node a = lane >> 2, points c and c + 4
+  const int a = r;
+  const double* o0 = sc + c * 20;
+  const double* o1 = sc + (c + 4) * 20;
+  double G0[3], G1[3];
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    G0[i] = o0[0 * 3 + i] * L[6] + o0[1 * 3 + i] * L[7] + o0[2 * 3 + i] * L[8];
+    G1[i] = o1[0 * 3 + i] * L[9] + o1[1 * 3 + i] * L[10] + o1[2 * 3 + i] * L[11];
+  }
+  const double w0 = o0[9], w1 = o1[9];
+  const int li = own[a];
+  if (P.rhs) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
+    double res[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        t = fma(o0[10 + i * 3 + j], G0[j], t);
+        t = fma(o1[10 + i * 3 + j], G1[j], t);
+      }
+      res[i] = -sum4(t);
+    }
+    if (c == 0 && li >= 0) {
+      double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        if constexpr (DET) racc[i * to.T] += res[i];
+        else atomicAdd(racc + i * to.T, res[i]);
+      }
+    }
+  }
+  if (P.values) {
+    double M[3][3][2];
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        M[j][k][0] = 0.0;
+        M[j][k][1] = 0.0;
+        dmma884(M[j][k], w0 * G0[j], G0[k]);
+        dmma884(M[j][k], w1 * G1[j], G1[k]);
+      }
+    if (li >= 0) {
+      const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li];
+      double* base = reinterpret_cast<double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[li];
+      const uint8_t* lc = sm + to.vloc + v * 64 + a * 8 + 2 * c;
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+        double* rowb = base + lc[t];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) {
+            const double kv = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+            if constexpr (DET) rowb[(i * 3 + m) * d] += kv;
+            else atomicAdd(rowb + (i * 3 + m) * d, kv);
+          }
+      }
+    }
+  }
+  __syncwarp();  // scratch is reused by the next visit
+}
+
 template <int KH, bool DET>
 __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_constant__ TiledParams P) {
   using C = TileCfg<ET_HEX, 1, KH, 2>;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   int* ctr = reinterpret_cast<int*>(smem + 64);
-  unsigned char* rbuf[2] = {smem + 128, smem + 128 + P.rec_cap};
-  double* hbuf[2];
-  hbuf[0] = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
-  hbuf[1] = hbuf[0] + P.hcap;
-  double* acc = hbuf[1] + P.hcap;
+  __shared__ TileOffs to;
+  __shared__ double lanetab[32 * LANE_TAB];
+#define RBUF(i) (smem + 128 + (size_t)(i) * P.rec_cap)
+#define HBUF(i) (reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap) + (size_t)(i) * P.hcap)
+  double* acc = HBUF(2);
   // facet-phase arrays (generic warp path)
   TileSmem F;
   unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
@@ -563,6 +717,19 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
   }
   const int tid = threadIdx.x, warp = tid >> 5;
   const GeoFrag GF = geo_frag();
+  if (warp == 0) {  // per-lane constant table (same for every warp)
+    double* Lt = lanetab + tid * LANE_TAB;
+#pragma unroll
+    for (int s = 0; s < 2; s++)
+#pragma unroll
+      for (int t = 0; t < 3; t++) Lt[s * 3 + t] = GF.b[s][t];
+    double g0[3], g1[3], N0, N1;
+    hex_ref(tid >> 2, tid & 3, g0, N0);
+    hex_ref(tid >> 2, (tid & 3) + 4, g1, N1);
+    for (int i = 0; i < 3; i++) { Lt[6 + i] = g0[i]; Lt[9 + i] = g1[i]; }
+    Lt[12] = N0;
+    Lt[13] = N1;
+  }
   int64_t tile = blockIdx.x;
   if (tile >= P.n_tiles) return;
   if (tid == 0) {
@@ -574,19 +741,19 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
   if (tid == 0) {
     const uint32_t bytes = (uint32_t)(P.rec_off[tile + 1] - P.rec_off[tile]);
     mbar_expect_tx(&mbar[0], bytes);
-    bulk_g2s(rbuf[0], P.rec + P.rec_off[tile], bytes, &mbar[0]);
+    bulk_g2s(RBUF(0), P.rec + P.rec_off[tile], bytes, &mbar[0]);
   }
   mbar_wait(&mbar[0], 0);
-  gather_halo(P, rbuf[0], hbuf[0]);
+  gather_halo(P, RBUF(0), HBUF(0));
   for (int it = 0; tile < P.n_tiles; it++, tile += gridDim.x) {
     const int cur = it & 1, oth = cur ^ 1;
     const int64_t next = tile + gridDim.x;
     if (tid == 0 && next < P.n_tiles) {  // prefetch the next record (its buffer was released last iteration)
       const uint32_t bytes = (uint32_t)(P.rec_off[next + 1] - P.rec_off[next]);
       mbar_expect_tx(&mbar[oth], bytes);
-      bulk_g2s(rbuf[oth], P.rec + P.rec_off[next], bytes, &mbar[oth]);
+      bulk_g2s(RBUF(oth), P.rec + P.rec_off[next], bytes, &mbar[oth]);
     }
-    const uint8_t* rec = rbuf[cur];
+    const uint8_t* rec = RBUF(cur);
     const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
     const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
     const uint32_t fmask = (uint32_t)hdr[5];
@@ -596,14 +763,24 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     V.vhal = reinterpret_cast<const uint16_t*>(rec + L.o_vhal);
     V.velem = reinterpret_cast<const int32_t*>(rec + L.o_velem);
     V.vloc = rec + L.o_vloc;
-    V.hdat = hbuf[cur];
+    V.hdat = HBUF(cur);
     V.H = H;
     V.tdeg = reinterpret_cast<const int32_t*>(rec + L.o_tdeg);
     V.toff = reinterpret_cast<const int32_t*>(rec + L.o_toff);
     V.acc = acc;
     V.racc = acc + acc_n;
     V.T = T;
-    if (tid == 0) *ctr = 0;
+    if (tid == 0) {
+      *ctr = 0;
+      const uint32_t rb = (uint32_t)(rec - smem);
+      to.vown = rb + L.o_vown; to.vhal = rb + L.o_vhal; to.velem = rb + L.o_velem; to.vloc = rb + L.o_vloc;
+      to.hdat = (uint32_t)(reinterpret_cast<const unsigned char*>(HBUF(cur)) - smem);
+      to.tdeg = rb + L.o_tdeg; to.toff = rb + L.o_toff;
+      to.acc = (uint32_t)(reinterpret_cast<unsigned char*>(acc) - smem);
+      to.racc = to.acc + 8u * (uint32_t)acc_n;
+      to.H = H;
+      to.T = T;
+    }
     for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
     cp_async_wait_all();
     __syncthreads();
@@ -612,20 +789,20 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     if constexpr (DET) {
       for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
         for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS) {
-          if constexpr (KH == 3) hex_visit_el<true>(P, V, Hc, GF, wsc, v);
+          if constexpr (KH == 3) hex_visit_el2<true>(P, to, Hc, lanetab, wsc, v, smem);
           else hex_visit<KH, true>(P, V, Hc, v);
         }
         __syncthreads();
       }
     } else {
       for (int v = warp; v < nv; v += C::WARPS) {  // hex visits are uniform: static split
-        if constexpr (KH == 3) hex_visit_el<false>(P, V, Hc, GF, wsc, v);
+        if constexpr (KH == 3) hex_visit_el2<false>(P, to, Hc, lanetab, wsc, v, smem);
         else hex_visit<KH, false>(P, V, Hc, v);
       }
     }
     if (next < P.n_tiles) {  // the next record has (almost surely) landed: start its halo gather
       mbar_wait(&mbar[oth], (uint32_t)(((it + 1) >> 1) & 1));
-      gather_halo(P, rbuf[oth], hbuf[oth]);
+      gather_halo(P, RBUF(oth), HBUF(oth));
     }
     // shared-memory view of the tile for the facet phase and the epilogue
     F.tnode = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(rec + L.o_tnode));
@@ -666,7 +843,7 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
   const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
-  if (smem > 227 * 1024) {
+  if (smem + 4096 > 227 * 1024) {  // + static shared memory (tile offsets, lane table)
     set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
     return FEM_E_UNSUPPORTED;
   }
