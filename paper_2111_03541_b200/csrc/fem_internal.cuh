@@ -65,13 +65,18 @@ struct TileSchedule {
 // Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by
 // 16-byte aligned sections (see rec_layout).  Built on the host at pattern time (loc on the device).
 struct RecLayout {
-  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, o_fcnt, o_fdv, o_ffac, size;
+  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, o_fcnt, o_fdv, o_ffac, o_fseg,
+      size;
 };
 // header[6] = number of boundary sets nb, header[7] = facet visits nf; facet visit i of set k
 // (fcnt[k] <= i < fcnt[k+1]) is facet ffac[i] of the tile's domain visit fdv[i].
-__host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, int nruns, int nb = 0, int nf = 0) {
+// header[8] = facet segments ns: fseg = int32 [nb+1] first segment of each set, then int32 [ns+1]
+// segment starts; the facets of one segment belong to distinct elements of one colour (node-disjoint),
+// so a deterministic kernel may run a segment's facets concurrently with plain adds.
+__host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, int nruns, int nb = 0, int nf = 0,
+                                                int ns = 0) {
   RecLayout L;
-  int o = 32;
+  int o = 48;
   auto al = [](int x) { return (x + 15) & ~15; };
   L.o_tnode = o; o = al(o + 4 * T);
   L.o_tdeg = o;  o = al(o + 4 * T);
@@ -86,11 +91,12 @@ __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, in
   L.o_fcnt = o;  o = al(o + 4 * (nb + 1));
   L.o_fdv = o;   o = al(o + 2 * nf);
   L.o_ffac = o;  o = al(o + nf);
+  L.o_fseg = o;  o = al(o + 4 * (nb + 1) + 4 * (ns + 1));
   L.size = o;
   return L;
 }
 __host__ __device__ inline RecLayout rec_layout_hdr(int NL, const int32_t* h) {
-  return rec_layout(NL, h[0], h[1], h[2], h[3], h[6], h[7]);
+  return rec_layout(NL, h[0], h[1], h[2], h[3], h[6], h[7], h[8]);
 }
 
 }  // namespace fem

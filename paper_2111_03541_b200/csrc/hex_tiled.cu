@@ -818,7 +818,8 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     F.vloc = V.vloc;
     F.hdat = const_cast<double*>(V.hdat);
     F.H = H;
-    if (fmask) rec_facets<ET_HEX, 1, KH, 2, FACET_WARPS>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
+    if (fmask)  // DET: node-disjoint facet segments, one barrier each
+      rec_facets<ET_HEX, 1, KH, 2, FACET_WARPS, DET>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
     tile_epilogue<KH>(P, F);
     __syncthreads();
   }

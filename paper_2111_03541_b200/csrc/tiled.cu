@@ -16,6 +16,7 @@
 // Only the element geometry of ghost-layer elements is recomputed; each (a,b) pair block is computed
 // exactly once (by the tile owning a).
 #include <algorithm>
+#include <tuple>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -44,8 +45,8 @@ static int64_t tile_halo_cap(int NL) {
 // its packed record (double-buffered in shared memory) would not fit: cap it at 4096 doubles.
 static int64_t acc_budget(int kh, int nl) {
   const char* s = getenv("FEM_TILE_ACC");
-  int64_t x = s ? atoll(s) : (kh == 1 ? 4096 : 16384);
-  (void)nl;
+  // P2 tets: 144 B of visit data per element, so the double-buffered records need room too
+  int64_t x = s ? atoll(s) : (kh == 1 ? 4096 : (nl == 10 ? 8192 : 16384));
   return x < 256 ? 256 : (x > ACC_BUDGET_MAX ? ACC_BUDGET_MAX : x);
 }
 
@@ -414,6 +415,50 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     std::vector<int32_t> halo;
     std::vector<int64_t> hoff(n_tiles + 1, 0);
     std::vector<int32_t> tmp;
+    // facet visits of tile t: per set, ordered by (rank of the facet among its element's facets in the set,
+    // domain visit, facet id), cut into segments of strictly increasing visits of one colour
+    std::vector<int16_t> f_dv;
+    std::vector<int8_t> f_fac;
+    std::vector<int32_t> f_cnt, f_segk, f_seg;
+    auto tile_facet_lists = [&](int64_t t) {
+      const int nv = (int)(dom_cnt[t + 1] - dom_cnt[t]);
+      const int nb = (int)fac_cnt.size();
+      f_dv.clear(); f_fac.clear(); f_cnt.assign(1, 0); f_segk.assign(1, 0); f_seg.clear();
+      if (nb == 0) { f_seg.push_back(0); return; }
+      std::vector<std::pair<int32_t, int16_t>> ev(nv);
+      for (int v = 0; v < nv; v++) ev[v] = {dom_items[dom_cnt[t] + v], (int16_t)v};
+      std::sort(ev.begin(), ev.end());
+      const int64_t r0 = dom_roff[t], nruns = dom_roff[t + 1] - r0;
+      auto colour_of = [&](int v) {  // run index of visit v
+        int r = 0;
+        while (r + 1 < nruns && dom_run[r0 + r + 1] - dom_cnt[t] <= v) r++;
+        return r;
+      };
+      std::vector<std::tuple<int, int16_t, int8_t>> items;
+      std::vector<int> seen(nv, 0);
+      for (int k = 0; k < nb; k++) {
+        items.clear();
+        for (int64_t j = fac_cnt[k][t]; j < fac_cnt[k][t + 1]; j++) {
+          const int32_t entry = fac_items[k][j];
+          const int32_t e = m->h_bset_elem[k][entry];
+          auto f = std::lower_bound(ev.begin(), ev.end(), std::make_pair(e, (int16_t)-32768));
+          items.emplace_back(seen[f->second]++, f->second, m->h_bset_facet[k][entry]);
+        }
+        for (auto& it : items) seen[std::get<1>(it)] = 0;
+        std::sort(items.begin(), items.end());
+        int prev_v = -1, prev_c = -1;
+        for (auto& it : items) {
+          const int v = std::get<1>(it), c = colour_of(v);
+          if (v <= prev_v || c != prev_c) f_seg.push_back((int32_t)f_dv.size());
+          prev_v = v; prev_c = c;
+          f_dv.push_back((int16_t)v);
+          f_fac.push_back(std::get<2>(it));
+        }
+        f_cnt.push_back((int32_t)f_dv.size());
+        f_segk.push_back((int32_t)f_seg.size());
+      }
+      f_seg.push_back((int32_t)f_dv.size());
+    };
     for (int64_t t = 0; t < n_tiles; t++) {
       const int64_t nvt = dom_cnt[t + 1] - dom_cnt[t];
       tmp.clear();
@@ -424,10 +469,9 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
       halo.insert(halo.end(), tmp.begin(), tmp.end());
       hoff[t + 1] = (int64_t)halo.size();
       const int nruns = (int)(dom_roff[t + 1] - dom_roff[t]);
-      int nf = 0;
-      for (size_t k = 0; k < fac_cnt.size(); k++) nf += (int)(fac_cnt[k][t + 1] - fac_cnt[k][t]);
+      tile_facet_lists(t);
       const RecLayout L = rec_layout(NL, (int)(tile_off[t + 1] - tile_off[t]), (int)tmp.size(), (int)nvt, nruns,
-                                     (int)fac_cnt.size(), nf);
+                                     (int)fac_cnt.size(), (int)f_dv.size(), (int)f_seg.size() - 1);
       roff[t + 1] = roff[t] + L.size;
       T.rec_max = std::max<int64_t>(T.rec_max, L.size);
     }
@@ -439,9 +483,9 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
       const int nv = (int)(dom_cnt[t + 1] - dom_cnt[t]);
       const int nruns = (int)(dom_roff[t + 1] - dom_roff[t]);
       const int nb = (int)fac_cnt.size();
-      int nf = 0;
-      for (int k = 0; k < nb; k++) nf += (int)(fac_cnt[k][t + 1] - fac_cnt[k][t]);
-      const RecLayout L = rec_layout(NL, Tn, H, nv, nruns, nb, nf);
+      tile_facet_lists(t);
+      const int nf = (int)f_dv.size(), ns = (int)f_seg.size() - 1;
+      const RecLayout L = rec_layout(NL, Tn, H, nv, nruns, nb, nf, ns);
       uint8_t* r = buf.data() + roff[t];
       int32_t* hdr = reinterpret_cast<int32_t*>(r);
       const int32_t* tn = tile_nodes.data() + tile_off[t];
@@ -461,26 +505,13 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
         o_toff[i + 1] = acc;
       }
       hdr[0] = Tn; hdr[1] = H; hdr[2] = nv; hdr[3] = nruns; hdr[4] = acc; hdr[5] = (int32_t)fac_mask[t];
-      hdr[6] = nb; hdr[7] = nf;
-      {  // facet visits: (domain visit of the facet's element, facet id)
-        std::vector<std::pair<int32_t, int16_t>> ev(nv);
-        for (int v = 0; v < nv; v++) ev[v] = {dom_items[dom_cnt[t] + v], (int16_t)v};
-        std::sort(ev.begin(), ev.end());
-        int32_t* o_fcnt = reinterpret_cast<int32_t*>(r + L.o_fcnt);
-        int16_t* o_fdv = reinterpret_cast<int16_t*>(r + L.o_fdv);
-        int8_t* o_ffac = reinterpret_cast<int8_t*>(r + L.o_ffac);
-        int i = 0;
-        for (int k = 0; k < nb; k++) {
-          o_fcnt[k] = i;
-          for (int64_t j = fac_cnt[k][t]; j < fac_cnt[k][t + 1]; j++, i++) {
-            const int32_t entry = fac_items[k][j];
-            const int32_t e = m->h_bset_elem[k][entry];
-            auto f = std::lower_bound(ev.begin(), ev.end(), std::make_pair(e, (int16_t)-32768));
-            o_fdv[i] = f->second;
-            o_ffac[i] = m->h_bset_facet[k][entry];
-          }
-        }
-        o_fcnt[nb] = i;
+      hdr[6] = nb; hdr[7] = nf; hdr[8] = ns;
+      if (nb > 0) {  // facet visits: (domain visit of the facet's element, facet id) + segments
+        memcpy(r + L.o_fcnt, f_cnt.data(), sizeof(int32_t) * f_cnt.size());
+        memcpy(r + L.o_fdv, f_dv.data(), sizeof(int16_t) * f_dv.size());
+        memcpy(r + L.o_ffac, f_fac.data(), f_fac.size());
+        memcpy(r + L.o_fseg, f_segk.data(), sizeof(int32_t) * f_segk.size());
+        memcpy(r + L.o_fseg + 4 * (nb + 1), f_seg.data(), sizeof(int32_t) * f_seg.size());
       }
       memcpy(r + L.o_hnode, hn, sizeof(int32_t) * H);
       int32_t* o_run = reinterpret_cast<int32_t*>(r + L.o_run);
@@ -752,12 +783,18 @@ int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_proble
   const int et = m->etype, o = m->order, kh = m->kh, q = prob->quad_order;
   if (et == ET_HEX && o == 1 && q == 2 && !getenv("FEM_NO_HEX_MMA")) {
     bool handled = false;
-    const int rc = launch_hex_tiled(P, T, kh, getenv("FEM_TILED_DET") != nullptr, s, &handled);
+    // colour-synchronous (bit-exact run to run) unless FEM_TILED_NONDET asks for the atomic variant
+    const int rc = launch_hex_tiled(P, T, kh, getenv("FEM_TILED_NONDET") == nullptr, s, &handled);
     if (handled) return rc;
   }
   if (et == ET_TET && o == 1 && kh == 4 && q == 2 && !getenv("FEM_NO_NS_SPEC")) {
     bool handled = false;
     const int rc = launch_ns_tiled(P, T, s, &handled);
+    if (handled) return rc;
+  }
+  if (et == ET_TET && o == 2 && kh == 3 && q == 2 && !getenv("FEM_NO_P2_SPEC")) {
+    bool handled = false;
+    const int rc = launch_p2_tiled(P, T, s, &handled);
     if (handled) return rc;
   }
   if (et == ET_TRI && o == 1) {

@@ -523,7 +523,7 @@ __device__ __forceinline__ int grab_visits(int* ctr, int step) {
 
 // Boundary terms from the tile record: facet visit i of set k is facet ffac[i] of domain visit fdv[i]
 // (the domain view D carries the staged halo and the local column offsets).
-template <int ET, int ORD, int KH, int Q, int NW>
+template <int ET, int ORD, int KH, int Q, int NW, bool DET = false>
 __device__ __forceinline__ void rec_facets(const TiledParams& P, const TileSmem& D, const uint8_t* rec,
                                            const RecLayout& L, unsigned char* slot) {
   const int32_t* fcnt = reinterpret_cast<const int32_t*>(rec + L.o_fcnt);
@@ -531,6 +531,22 @@ __device__ __forceinline__ void rec_facets(const TiledParams& P, const TileSmem&
   const int8_t* ffac = reinterpret_cast<const int8_t*>(rec + L.o_ffac);
   const int warp = threadIdx.x >> 5;
   __syncthreads();  // per-warp slots may alias scratch used by the domain phase
+  if constexpr (DET) {
+    // segment by segment (node-disjoint facets, see rec_layout): each accumulator entry receives at
+    // most one contribution per segment, from one lane, so the summation order is fixed
+    const int32_t* segk = reinterpret_cast<const int32_t*>(rec + L.o_fseg);
+    const int32_t* seg = segk + reinterpret_cast<const int32_t*>(rec)[6] + 1;
+    for (int f = 0; f < P.n_fac; f++) {
+      const int k = P.fac_set[f];
+      for (int sg = segk[k]; sg < segk[k + 1]; sg++) {
+        if (warp < NW)
+          for (int i = seg[sg] + warp; i < seg[sg + 1]; i += NW)
+            warp_visit<ET, ORD, KH, Q, true, false>(P, &P.fac[f], 1, D, fdv[i], slot, ffac[i]);
+        __syncthreads();
+      }
+    }
+    return;
+  }
   if (warp >= NW) return;
   for (int f = 0; f < P.n_fac; f++) {
     const int k = P.fac_set[f];
@@ -590,5 +606,6 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled);
 int launch_ns_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled);
+int launch_p2_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled);
 
 }  // namespace fem

@@ -74,9 +74,10 @@ def test_small_parity_all_modes(name, variant):
     S.close()
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-@pytest.mark.parametrize("sc", ["coloured"])
+@pytest.mark.parametrize("name,sc", [(n, "coloured") for n in ("c2", "c3", "c4", "c5")] +
+                         [("c2", "tiled"), ("c5", "tiled")])
 def test_deterministic_modes_bit_exact(name, sc):
+    """Coloured scatter everywhere, and the tiled path on Q1 hex (colour-synchronous visits)."""
     _need_gpu()
     m, p = make_config(name, "perturbed", SMALL[name])
     st = _to_dev(make_state(name, m, p))
