@@ -44,6 +44,22 @@ def _peaks():
 
 
 FP64_PEAK_TFLOPS = 33.0  # measured DFMA peak on this pool's B200 (profiles/r01_m0_microbench.txt)
+DMMA_PEAK_TFLOPS = 36.0  # measured fp64 DMMA m8n8k4 peak (profiles/r01_m0b_dmma_smem.txt)
+
+# the record-driven kernel the tiled path launches per configuration (csrc/tiled.cu launch_tiled)
+TILED_KERNEL = {"c1": "k_tiled<TRI,P1>", "c2": "k_hex_rec<1,DET>", "c3": "k_p2_rec", "c4": "k_ns_rec",
+                "c5": "k_hex_rec<3,DET>"}
+
+
+def _traffic(name, variant, scatter):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel from the committed
+    `ncu --set full` capture (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)[f"{name}/{variant}/{scatter}"]
+        return float(t["dram_bytes"]), t["source"]
+    except Exception:
+        return None, None
 
 
 class ClockSampler:
@@ -254,6 +270,7 @@ def main():
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
         alg_bytes = algorithmic_bytes(mesh, prob, nnz_total, S.kh * mesh.n_nodes)
         achieved = alg_bytes / (kern_ms * 1e-3) / 1e9 / world
+        traffic, traffic_src = _traffic(name, args.variant, args.scatter) if world == 1 else (None, None)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             r = run_oracle_steps(name, 1, 0)
@@ -270,10 +287,13 @@ def main():
             "nnz_per_s": nnz_total / (ms * 1e-3),
             "pattern_build_s": t_pattern,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "peak_kind": f"{peak_kind} hbm_gbs", "algorithmic_bytes_per_step": alg_bytes,
-                         "kernel": "k_tiled (fem_assemble_system, FEM_SCATTER_TILED)"},
-            "fp64": {"peak_tflops": FP64_PEAK_TFLOPS, "peak_kind": "measured DFMA (tools/m0)"},
+                         "kernel": (TILED_KERNEL[name] if args.scatter == "tiled" else f"{args.scatter} kernels")
+                         + " (fem_assemble_system)"},
+            "fp64": {"peak_tflops": FP64_PEAK_TFLOPS, "peak_kind": "measured DFMA (tools/m0)",
+                     "dmma_peak_tflops": DMMA_PEAK_TFLOPS},
             "cpu_baseline": cpu,
             "e2e": {"value": E_total / (e2e_ms * 1e-3), "unit": "elements/s",
                     "h2d_bytes_per_step": int(state.nbytes), "d2h_bytes_per_step": 16,

@@ -65,11 +65,13 @@ struct TileSchedule {
 // Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by
 // 16-byte aligned sections (see rec_layout).  Built on the host at pattern time (loc on the device).
 struct RecLayout {
-  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, o_fcnt, o_fdv, o_ffac, o_fseg,
-      size;
+  int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, o_vseq, o_fcnt, o_fdv, o_ffac,
+      o_fseg, size;
 };
 // header[6] = number of boundary sets nb, header[7] = facet visits nf; facet visit i of set k
 // (fcnt[k] <= i < fcnt[k+1]) is facet ffac[i] of the tile's domain visit fdv[i].
+// vseq[v][a] = number of earlier visits of the record that touch node a (u8, saturating at 255): the
+// turn of visit v on the accumulator row of a in the ordered deterministic kernels.
 // header[8] = facet segments ns: fseg = int32 [nb+1] first segment of each set, then int32 [ns+1]
 // segment starts; the facets of one segment belong to distinct elements of one colour (node-disjoint),
 // so a deterministic kernel may run a segment's facets concurrently with plain adds.
@@ -88,6 +90,7 @@ __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, in
   L.o_vhal = o;  o = al(o + 2 * nv * NL);
   L.o_vown = o;  o = al(o + 2 * nv * NL);
   L.o_vloc = o;  o = al(o + nv * NL * NL);
+  L.o_vseq = o;  o = al(o + nv * NL);
   L.o_fcnt = o;  o = al(o + 4 * (nb + 1));
   L.o_fdv = o;   o = al(o + 2 * nf);
   L.o_ffac = o;  o = al(o + nf);

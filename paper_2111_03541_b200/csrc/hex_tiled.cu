@@ -530,14 +530,14 @@ __device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t*
 // Offsets (bytes from the dynamic shared-memory base) of the current tile's arrays: kept in shared
 // memory so every visit addresses them with LDS and without rematerialising the record layout.
 struct TileOffs {
-  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc;
+  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc, vseq, turn;
   int H, T;
 };
 // Per-lane constants of the fragment layout: B fragments of the geometry GEMM (6), ∇̂N_a at points c
 // and c+4 (6), N_a at c and c+4 (2); lane l = 4a + c.
 constexpr int LANE_TAB = 14;
 
-template <bool DET>
+template <bool DET, bool ORDERED = DET>
 __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOffs& to, const HexCoef& H,
                                               const double* __restrict__ lt, double* sc, int v,
                                               unsigned char* sm) {
@@ -583,6 +583,15 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     if (lane == 0)
       atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL),
                 (unsigned long long)reinterpret_cast<const int32_t*>(sm + to.velem)[v]);
+    if constexpr (ORDERED) {  // still pass the turn on, or later visits of these rows would wait forever
+      const int li = own[r];
+      if (c == 0 && li >= 0) {
+        volatile int* tp = reinterpret_cast<volatile int*>(sm + to.turn) + li;
+        const int t = (sm + to.vseq)[v * 8 + r];
+        while (*tp != t) __nanosleep(64);
+        *tp = t + 1;
+      }
+    }
     __syncwarp();
     return;
   }
@@ -627,8 +636,9 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   }
   const double w0 = o0[9], w1 = o1[9];
   const int li = own[a];
+  // the residual rows first (three registers), then the turn, the Gram blocks and the writes
+  double res[3] = {0.0, 0.0, 0.0};
   if (P.rhs) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
-    double res[3];
 #pragma unroll
     for (int i = 0; i < 3; i++) {
       double t = 0.0;
@@ -639,13 +649,23 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       }
       res[i] = -sum4(t);
     }
-    if (c == 0 && li >= 0) {
-      double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
+  }
+  int* turn = reinterpret_cast<int*>(sm + to.turn);
+  int my_turn = 0;
+  if constexpr (ORDERED) {  // wait for this visit's turn on the owned row it writes (record order)
+    if (li >= 0) {
+      my_turn = (sm + to.vseq)[v * 8 + a];
+      while (*reinterpret_cast<volatile int*>(turn + li) != my_turn)
+        if (P.spin_ns) __nanosleep(P.spin_ns);
+    }
+    __threadfence_block();
+  }
+  if (P.rhs && c == 0 && li >= 0) {
+    double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
 #pragma unroll
-      for (int i = 0; i < 3; i++) {
-        if constexpr (DET) racc[i * to.T] += res[i];
-        else atomicAdd(racc + i * to.T, res[i]);
-      }
+    for (int i = 0; i < 3; i++) {
+      if constexpr (DET) racc[i * to.T] += res[i];
+      else atomicAdd(racc + i * to.T, res[i]);
     }
   }
   if (P.values) {
@@ -678,7 +698,11 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       }
     }
   }
-  __syncwarp();  // scratch is reused by the next visit
+  __syncwarp();  // scratch is reused by the next visit; the row's four lanes have written
+  if constexpr (ORDERED) {  // hand the row to the next visit in record order
+    __threadfence_block();
+    if (c == 0 && li >= 0) *reinterpret_cast<volatile int*>(turn + li) = my_turn + 1;
+  }
 }
 
 template <int KH, bool DET>
@@ -694,7 +718,8 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
   double* acc = HBUF(2);
   // facet-phase arrays (generic warp path)
   TileSmem F;
-  unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
+  int* turn = reinterpret_cast<int*>(acc + P.acc_cap);
+  unsigned char* fp = reinterpret_cast<unsigned char*>(turn + P.turn_cap);
   F.qp = fp;
   fp += std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS);
   F.vid = reinterpret_cast<int32_t*>(fp);
@@ -778,18 +803,26 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
       to.tdeg = rb + L.o_tdeg; to.toff = rb + L.o_toff;
       to.acc = (uint32_t)(reinterpret_cast<unsigned char*>(acc) - smem);
       to.racc = to.acc + 8u * (uint32_t)acc_n;
+      to.vseq = rb + L.o_vseq;
+      to.turn = (uint32_t)(reinterpret_cast<unsigned char*>(turn) - smem);
       to.H = H;
       to.T = T;
     }
     for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
+    if constexpr (DET)
+      for (int i = tid; i < T; i += blockDim.x) turn[i] = 0;
     cp_async_wait_all();
     __syncthreads();
     const int32_t* run = reinterpret_cast<const int32_t*>(rec + L.o_run);
     double* wsc = reinterpret_cast<double*>(F.qp) + (size_t)HEX_SCRATCH * warp;
-    if constexpr (DET) {
+    if (DET && KH == 3 && !P.det_runs) {
+      // ordered: visit v takes its turn on each accumulator row it writes (vseq), so every entry sums its
+      // contributions in record order with plain adds, without block-wide barriers between colours
+      for (int v = warp; v < nv; v += C::WARPS) hex_visit_el2<DET>(P, to, Hc, lanetab, wsc, v, smem);
+    } else if constexpr (DET) {
       for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
         for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS) {
-          if constexpr (KH == 3) hex_visit_el2<true>(P, to, Hc, lanetab, wsc, v, smem);
+          if constexpr (KH == 3) hex_visit_el2<true, false>(P, to, Hc, lanetab, wsc, v, smem);
           else hex_visit<KH, true>(P, V, Hc, v);
         }
         __syncthreads();
@@ -842,8 +875,11 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
   P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)KH * T.max_tile_nodes);
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
+  P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
+  P.spin_ns = getenv("FEM_SPIN_NS") ? atoi(getenv("FEM_SPIN_NS")) : 0;
+  P.det_runs = getenv("FEM_DET_RUNS") != nullptr;
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
-  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
+  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + fac_bytes;
   if (smem + 4096 > 227 * 1024) {  // + static shared memory (tile offsets, lane table)
     set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
     return FEM_E_UNSUPPORTED;

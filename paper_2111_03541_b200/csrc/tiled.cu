@@ -519,6 +519,8 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
       int32_t* o_velem = reinterpret_cast<int32_t*>(r + L.o_velem);
       uint16_t* o_vhal = reinterpret_cast<uint16_t*>(r + L.o_vhal);
       int16_t* o_vown = reinterpret_cast<int16_t*>(r + L.o_vown);
+      uint8_t* o_vseq = r + L.o_vseq;
+      std::vector<int> turn(Tn, 0);
       for (int v = 0; v < nv; v++) {
         const int64_t gi = dom_cnt[t] + v;
         const int32_t e = dom_items[gi];
@@ -528,6 +530,7 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
           o_vhal[v * NL + a] = (uint16_t)(std::lower_bound(hn, hn + H, node) - hn);
           const int32_t* f = std::lower_bound(tn, tn + Tn, node);
           o_vown[v * NL + a] = (f != tn + Tn && *f == node) ? (int16_t)(f - tn) : (int16_t)-1;
+          o_vseq[v * NL + a] = o_vown[v * NL + a] >= 0 ? (uint8_t)std::min(turn[f - tn]++, 255) : (uint8_t)0;
         }
         vis_loc[gi] = roff[t] + L.o_vloc + (int64_t)v * NL * NL;
       }

@@ -46,6 +46,9 @@ struct TiledParams {
   int rec_cap;   // bytes of one record buffer
   int hcap;      // doubles of one halo buffer
   int acc_cap;   // doubles of the accumulator (incl. residual rows)
+  int turn_cap;  // ints of the per-row turn counters (ordered deterministic kernels), multiple of 4
+  int spin_ns;   // back-off of a visit waiting for its turn (FEM_SPIN_NS, default 0 = spin)
+  int det_runs;  // deterministic hex: colour runs + barriers instead of per-row turns (FEM_DET_RUNS)
   int fvmax;     // capacity of the facet visit arrays
 };
 
