@@ -98,6 +98,13 @@ __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, in
   L.size = o;
   return L;
 }
+// Accumulator row stride of a tile point with d block columns: entry (i, m, col) of its KH x KH blocks
+// sits at toff + i*stride + m*d + col.  One pad double when needed makes stride ≡ KH*nnz_s (mod 2), so
+// that with toff ≡ KH*rowptr_s (mod 2) every row segment has the 16-byte phase of its destination in
+// `values` and can leave by one bulk (TMA) store.
+__host__ __device__ inline int acc_row_stride(int KH, int d, int64_t nnz_s) {
+  return KH == 1 ? d : KH * d + ((KH * (d + (int)(nnz_s & 1))) & 1);
+}
 __host__ __device__ inline RecLayout rec_layout_hdr(int NL, const int32_t* h) {
   return rec_layout(NL, h[0], h[1], h[2], h[3], h[6], h[7], h[8]);
 }

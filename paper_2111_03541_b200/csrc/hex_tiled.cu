@@ -262,7 +262,7 @@ __device__ __forceinline__ void hex_visit(const TiledParams& P, const HexView& S
       for (int t = 0; t < 2; t++) Kb[t][0][0] = -(H.kf0 * M[t] + H.Cf1 * Mm[t]);
     }
     if (li >= 0) {
-      const int d = S.tdeg[li];
+      const int d = S.tdeg[li], sr = acc_row_stride(KH, d, P.nnz_s);
       double* base = S.acc + S.toff[li];
 #pragma unroll
       for (int t = 0; t < 2; t++) {
@@ -273,8 +273,8 @@ __device__ __forceinline__ void hex_visit(const TiledParams& P, const HexView& S
         for (int i = 0; i < KH; i++)
 #pragma unroll
           for (int m = 0; m < KH; m++) {
-            if constexpr (DET) rowb[(i * KH + m) * d] += Kb[t][i][m];
-            else atomicAdd(rowb + (i * KH + m) * d, Kb[t][i][m]);
+            if constexpr (DET) rowb[i * sr + m * d] += Kb[t][i][m];
+            else atomicAdd(rowb + i * sr + m * d, Kb[t][i][m]);
           }
       }
     }
@@ -491,7 +491,7 @@ __device__ __forceinline__ void hex_visit_el(const TiledParams& P, const HexView
         dmma884(M[j][k], w1 * G1[j], G1[k]);
       }
     if (li >= 0) {
-      const int d = S.tdeg[li];
+      const int d = S.tdeg[li], sr = acc_row_stride(3, d, P.nnz_s);
       double* base = S.acc + S.toff[li];
       const uint8_t* lc = S.vloc + v * 64 + a * 8 + 2 * c;
 #pragma unroll
@@ -503,8 +503,8 @@ __device__ __forceinline__ void hex_visit_el(const TiledParams& P, const HexView
 #pragma unroll
           for (int m = 0; m < 3; m++) {
             const double kv = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
-            if constexpr (DET) rowb[(i * 3 + m) * d] += kv;
-            else atomicAdd(rowb + (i * 3 + m) * d, kv);
+            if constexpr (DET) rowb[i * sr + m * d] += kv;
+            else atomicAdd(rowb + i * sr + m * d, kv);
           }
       }
     }
@@ -680,21 +680,29 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
         dmma884(M[j][k], w1 * G1[j], G1[k]);
       }
     if (li >= 0) {
-      const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li];
+      const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li], sr = acc_row_stride(3, d, P.nnz_s);
       double* base = reinterpret_cast<double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[li];
       const uint8_t* lc = sm + to.vloc + v * 64 + a * 8 + 2 * c;
 #pragma unroll
       for (int t = 0; t < 2; t++) {
         const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
         double* rowb = base + lc[t];
+        if constexpr (DET) {  // nine independent read-modify-writes: loads first (d may alias for the compiler)
+          double old[9];
 #pragma unroll
-        for (int i = 0; i < 3; i++)
+          for (int e = 0; e < 9; e++) old[e] = rowb[(e / 3) * sr + (e % 3) * d];
 #pragma unroll
-          for (int m = 0; m < 3; m++) {
-            const double kv = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
-            if constexpr (DET) rowb[(i * 3 + m) * d] += kv;
-            else atomicAdd(rowb + (i * 3 + m) * d, kv);
-          }
+          for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int m = 0; m < 3; m++)
+              rowb[i * sr + m * d] = old[i * 3 + m] - (H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int m = 0; m < 3; m++)
+              atomicAdd(rowb + i * sr + m * d, -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0)));
+        }
       }
     }
   }
@@ -808,7 +816,8 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
       to.H = H;
       to.T = T;
     }
-    for (int i = tid; i < acc_n + KH * T; i += blockDim.x) acc[i] = 0.0;
+    for (int i = tid; i < (acc_n + KH * T + 1) / 2; i += blockDim.x)  // acc is 16-byte aligned, acc_cap even
+      reinterpret_cast<double2*>(acc)[i] = make_double2(0.0, 0.0);
     if constexpr (DET)
       for (int i = tid; i < T; i += blockDim.x) turn[i] = 0;
     cp_async_wait_all();

@@ -159,12 +159,12 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
   }
   if (valid && li >= 0) {
     if (P.values) {
-      const int d = D.tdeg[li];
+      const int d = D.tdeg[li], sr = acc_row_stride(4, d, P.nnz_s);
       double* rowb = D.acc + D.toff[li] + D.vloc[vv * 16 + a * 4 + b];
 #pragma unroll
       for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int m = 0; m < 4; m++) atomicAdd(rowb + (i * 4 + m) * d, c.f0 * acc[i][m]);
+        for (int m = 0; m < 4; m++) atomicAdd(rowb + i * sr + m * d, c.f0 * acc[i][m]);
     }
     if (P.rhs) atomicAdd(D.racc + b * D.T + li, res);
   }

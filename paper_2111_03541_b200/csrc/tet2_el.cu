@@ -176,7 +176,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
   // tile 1: rows a0, columns b = 2c + t
   gram(G0, G0);
   if (li0 >= 0) {
-    const int d = tdeg[li0];
+    const int d = tdeg[li0], sr = acc_row_stride(3, d, P.nnz_s);
     double* base = acc + toff[li0];
 #pragma unroll
     for (int t = 0; t < 2; t++) {
@@ -185,7 +185,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
-        for (int m = 0; m < 3; m++) atomicAdd(rowb + (i * 3 + m) * d, kval(i, m, t, tr));
+        for (int m = 0; m < 3; m++) atomicAdd(rowb + i * sr + m * d, kval(i, m, t, tr));
     }
   }
   // tile 2: pair (a0, 8 + t); c < 2 writes block (a0, 8 + c), c >= 2 the transposed block (8 + c - 2, a0)
@@ -203,13 +203,13 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
     if (li >= 0) {
       const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
       double* rowb = acc + toff[li] + vloc[ra * 10 + cb];
-      const int d = tdeg[li];
+      const int d = tdeg[li], sr = acc_row_stride(3, d, P.nnz_s);
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int m = 0; m < 3; m++) {
           const double kv = -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0));
-          atomicAdd(rowb + (tr_blk ? (m * 3 + i) : (i * 3 + m)) * d, kv);
+          atomicAdd(rowb + (tr_blk ? m * sr + i * d : i * sr + m * d), kv);
         }
     }
   }
@@ -224,12 +224,12 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
       for (int k = 0; k < 3; k++) Ms[j][k] = t ? M[j][k][1] : M[j][k][0];
     const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
     double* rowb = acc + toff[li1] + vloc[a1 * 10 + 8 + t];
-    const int d = tdeg[li1];
+    const int d = tdeg[li1], sr = acc_row_stride(3, d, P.nnz_s);
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
       for (int m = 0; m < 3; m++)
-        atomicAdd(rowb + (i * 3 + m) * d, -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0)));
+        atomicAdd(rowb + i * sr + m * d, -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0)));
   }
   __syncwarp();
 }

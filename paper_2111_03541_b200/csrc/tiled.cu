@@ -172,7 +172,7 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   for (int64_t i = 0; i < n_own; i++) {
     const int64_t deg = rps[i + 1] - rps[i];
     if (deg > 255) { set_error("tiled schedule: a row has more than 255 scalar neighbours"); return FEM_E_UNSUPPORTED; }
-    sz[i] = (int64_t)KH * KH * deg;
+    sz[i] = (int64_t)KH * acc_row_stride(KH, (int)deg, p->nnz_s) + 1;  // + phase pad
     max_sz = std::max(max_sz, sz[i]);
   }
   const int64_t ACC_BUDGET = acc_budget(KH, NL);
@@ -495,15 +495,16 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
       int32_t* o_toff = reinterpret_cast<int32_t*>(r + L.o_toff);
       int64_t* o_trps = reinterpret_cast<int64_t*>(r + L.o_trps);
       int acc = 0;
-      o_toff[0] = 0;
       for (int i = 0; i < Tn; i++) {
         const int64_t li = tn[i] - lo;
         o_tnode[i] = tn[i];
         o_trps[i] = rps[li];
         o_tdeg[i] = (int32_t)(rps[li + 1] - rps[li]);
-        acc += KH * KH * o_tdeg[i];
-        o_toff[i + 1] = acc;
+        if ((acc ^ (int)((KH * rps[li]) & 1)) & 1) acc++;  // 16-byte phase of the destination rows
+        o_toff[i] = acc;
+        acc += KH * acc_row_stride(KH, o_tdeg[i], p->nnz_s);
       }
+      o_toff[Tn] = acc;
       hdr[0] = Tn; hdr[1] = H; hdr[2] = nv; hdr[3] = nruns; hdr[4] = acc; hdr[5] = (int32_t)fac_mask[t];
       hdr[6] = nb; hdr[7] = nf; hdr[8] = ns;
       if (nb > 0) {  // facet visits: (domain visit of the facet's element, facet id) + segments

@@ -368,12 +368,12 @@ __device__ __forceinline__ void warp_visit(const TiledParams& P, const FormArgs*
         for (int f = 0; f < nforms; f++)
           if (forms[f].form != FEM_WF_ELAST_LOAD) pair_block<DIM, NL, KH, NQ>(forms[f], qg, a, b, K);
       }
-      const int d = S.tdeg[li];
+      const int d = S.tdeg[li], sr = acc_row_stride(KH, d, P.nnz_s);
       double* rowb = S.acc + S.toff[li] + pos;
 #pragma unroll
       for (int i = 0; i < KH; i++)
 #pragma unroll
-        for (int m = 0; m < KH; m++) atomicAdd(rowb + (i * KH + m) * d, K[i][m]);
+        for (int m = 0; m < KH; m++) atomicAdd(rowb + i * sr + m * d, K[i][m]);
     } else {
       double rr[KH];
 #pragma unroll
@@ -487,7 +487,7 @@ __device__ __forceinline__ void tile_prologue(const TiledParams& P, TileSmem& S,
     int carry = 0;
     for (int base = 0; base < T; base += 32) {
       const int i = base + tid;
-      int v = (i < T) ? KH * KH * S.tdeg[i] : 0;
+      int v = (i < T) ? KH * acc_row_stride(KH, S.tdeg[i], P.nnz_s) : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int u = __shfl_up_sync(0xffffffffu, v, o);
@@ -558,19 +558,51 @@ __device__ __forceinline__ void rec_facets(const TiledParams& P, const TileSmem&
   }
 }
 
-// write every owned row once (coalesced, one warp per row) and the residual rows
+// bulk (TMA) store shared -> global, completion tracked per thread by bulk groups
+__device__ __forceinline__ void bulk_s2g(double* dst, const double* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Write every owned row once and the residual rows.  A row segment whose shared-memory copy has the
+// 16-byte phase of its destination (the record layout arranges it, see acc_row_stride) leaves by one
+// bulk store of its aligned middle plus at most two single doubles; other rows are copied by a warp.
+// The bulk stores drain to HBM asynchronously; only their shared-memory reads are awaited (before the
+// accumulator is reused).
 template <int KH>
 __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const TileSmem& S) {
+  fence_proxy_async_smem();  // generic-proxy accumulator writes -> async-proxy (bulk copy) reads
   __syncthreads();
   const int tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, T = S.T;
+  const int lane = tid & 31, nw = nth >> 5;
   if (P.values) {
-    const int lane = tid & 31, nw = nth >> 5;
+    bool issued = false;
     for (int rr = warp; rr < T * KH; rr += nw) {
       const int li = rr / KH, k0 = rr % KH;
-      const int len = KH * S.tdeg[li];
-      const double* src = S.acc + S.toff[li] + k0 * len;
+      const int d = S.tdeg[li];
+      const int len = KH * d;
+      const double* src = S.acc + S.toff[li] + k0 * acc_row_stride(KH, d, P.nnz_s);
       double* dst = P.values + (int64_t)k0 * KH * P.nnz_s + (int64_t)KH * S.trps[li];
-      for (int j = lane; j < len; j += 32) dst[j] = src[j];
+      if ((((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0 && len >= 4) {
+        const int head = ((uintptr_t)dst & 15) ? 1 : 0;
+        const int mid = (len - head) & ~1;
+        if (lane == 0) {
+          bulk_s2g(dst + head, src + head, 8u * (uint32_t)mid);
+          issued = true;
+        }
+        if (lane == 1 && head) dst[0] = src[0];
+        if (lane == 2 && head + mid < len) dst[len - 1] = src[len - 1];
+      } else {
+        for (int j = lane; j < len; j += 32) dst[j] = src[j];
+      }
+    }
+    if (issued) {
+      bulk_commit();
+      bulk_wait_read_all();  // the accumulator may be zeroed for the next tile after the caller's barrier
     }
   }
   if (P.rhs)
