@@ -713,8 +713,14 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   }
 }
 
+#ifndef FEM_HEX_THREADS
+#define FEM_HEX_THREADS 512
+#endif
+constexpr int HEX_THREADS = FEM_HEX_THREADS;  // threads of the persistent hex kernel
+constexpr int HEX_WARPS = HEX_THREADS / 32;
+
 template <int KH, bool DET>
-__global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_constant__ TiledParams P) {
+__global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constant__ TiledParams P) {
   using C = TileCfg<ET_HEX, 1, KH, 2>;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
@@ -729,7 +735,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
   int* turn = reinterpret_cast<int*>(acc + P.acc_cap);
   unsigned char* fp = reinterpret_cast<unsigned char*>(turn + P.turn_cap);
   F.qp = fp;
-  fp += std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS);
+  fp += std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * HEX_WARPS);
   F.vid = reinterpret_cast<int32_t*>(fp);
   fp += 4 * (size_t)P.fvmax;
   F.vnode = reinterpret_cast<int32_t*>(fp);
@@ -827,17 +833,20 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_rec(const __grid_const
     if (DET && KH == 3 && !P.det_runs) {
       // ordered: visit v takes its turn on each accumulator row it writes (vseq), so every entry sums its
       // contributions in record order with plain adds, without block-wide barriers between colours
-      for (int v = warp; v < nv; v += C::WARPS) hex_visit_el2<DET>(P, to, Hc, lanetab, wsc, v, smem);
+      if (P.hex_dyn)  // visits are taken in increasing order, so every awaited turn belongs to a running visit
+        for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) hex_visit_el2<DET>(P, to, Hc, lanetab, wsc, v, smem);
+      else
+        for (int v = warp; v < nv; v += HEX_WARPS) hex_visit_el2<DET>(P, to, Hc, lanetab, wsc, v, smem);
     } else if constexpr (DET) {
       for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
-        for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS) {
+        for (int v = run[r] + warp; v < run[r + 1]; v += HEX_WARPS) {
           if constexpr (KH == 3) hex_visit_el2<true, false>(P, to, Hc, lanetab, wsc, v, smem);
           else hex_visit<KH, true>(P, V, Hc, v);
         }
         __syncthreads();
       }
     } else {
-      for (int v = warp; v < nv; v += C::WARPS) {  // hex visits are uniform: static split
+      for (int v = warp; v < nv; v += HEX_WARPS) {  // hex visits are uniform: static split
         if constexpr (KH == 3) hex_visit_el2<false>(P, to, Hc, lanetab, wsc, v, smem);
         else hex_visit<KH, false>(P, V, Hc, v);
       }
@@ -887,7 +896,8 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
   P.spin_ns = getenv("FEM_SPIN_NS") ? atoi(getenv("FEM_SPIN_NS")) : 0;
   P.det_runs = getenv("FEM_DET_RUNS") != nullptr;
-  const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * C::WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
+  P.hex_dyn = getenv("FEM_HEX_DYN") != nullptr;
+  const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * HEX_WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
   const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + fac_bytes;
   if (smem + 4096 > 227 * 1024) {  // + static shared memory (tile offsets, lane table)
     set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
@@ -899,7 +909,7 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
-  k_hex_rec<KH, DET><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  k_hex_rec<KH, DET><<<(unsigned)grid, HEX_THREADS, smem, s>>>(P);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfem.so")
+LIB_PATH = os.environ.get("FEM_LIB_PATH") or os.path.join(_HERE, "libfem.so")  # override: dev A/B builds
 
 FEM_TRI, FEM_TET, FEM_HEX = 1, 2, 4
 FEM_THERMAL, FEM_ELASTICITY, FEM_NS = 1, 2, 3
