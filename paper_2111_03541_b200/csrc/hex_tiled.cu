@@ -548,6 +548,7 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   const int HH = to.H;
   const int c = lane & 3, r = lane >> 2;
   const double* L = lt + lane * LANE_TAB;
+  const bool kd = P.values && P.rhs;  // system call: residual as K'·d (below), no stress at the points
   // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
   double C3[3][2];
 #pragma unroll
@@ -606,22 +607,24 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
     Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
     Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
-    double gu[3][3];
-#pragma unroll
-    for (int k = 0; k < 3; k++)
-#pragma unroll
-      for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
     double* o = sc + q * 20;  // per-point records (the GEMM output has been consumed)
 #pragma unroll
     for (int j = 0; j < 3; j++)
 #pragma unroll
       for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
     o[9] = det;  // w (unit Gauss-Legendre weights)
-    const double lw = H.sl * det * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * det;
+    if (!kd) {  // stress at the point for the residual-only call
+      double gu[3][3];
 #pragma unroll
-    for (int i = 0; i < 3; i++)
+      for (int k = 0; k < 3; k++)
 #pragma unroll
-      for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+        for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+      const double lw = H.sl * det * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * det;
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+    }
   }
   __syncwarp();
   // ---- fragment layout: node a = lane >> 2, points c and c + 4
@@ -636,9 +639,9 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   }
   const double w0 = o0[9], w1 = o1[9];
   const int li = own[a];
-  // the residual rows first (three registers), then the turn, the Gram blocks and the writes
+  // residual-only call: the residual rows first (three registers), then the turn and the writes
   double res[3] = {0.0, 0.0, 0.0};
-  if (P.rhs) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
+  if (P.rhs && !kd) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
 #pragma unroll
     for (int i = 0; i < 3; i++) {
       double t = 0.0;
@@ -660,15 +663,19 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     }
     __threadfence_block();
   }
-  if (P.rhs && c == 0 && li >= 0) {
-    double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
+  auto write_res = [&]() {
+    if (P.rhs && c == 0 && li >= 0) {
+      double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
 #pragma unroll
-    for (int i = 0; i < 3; i++) {
-      if constexpr (DET) racc[i * to.T] += res[i];
-      else atomicAdd(racc + i * to.T, res[i]);
+      for (int i = 0; i < 3; i++) {
+        if constexpr (DET) racc[i * to.T] += res[i];
+        else atomicAdd(racc + i * to.T, res[i]);
+      }
     }
-  }
-  if (P.values) {
+  };
+  if (!P.values) {
+    write_res();
+  } else {
     double M[3][3][2];
 #pragma unroll
     for (int j = 0; j < 3; j++)
@@ -679,6 +686,23 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
         dmma884(M[j][k], w0 * G0[j], G0[k]);
         dmma884(M[j][k], w1 * G1[j], G1[k]);
       }
+    if (kd) {  // the form is linear in d: r_(a,i) = Σ_(b,m) K'_(a,i),(b,m) d_(b,m), K' = K at f0 = 1
+      const uint16_t* hb = hv + 2 * c;
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        double t_ = 0.0;
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+          const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+#pragma unroll
+          for (int m = 0; m < 3; m++)
+            t_ = fma(-(H.sl * M[i][m][t] + H.sm * M[m][i][t] + (i == m ? H.sm * tr : 0.0)),
+                     hdat[(3 + m) * HH + hb[t]], t_);
+        }
+        res[i] = sum4(t_);
+      }
+    }
+    write_res();
     if (li >= 0) {
       const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li], sr = acc_row_stride(3, d, P.nnz_s);
       double* base = reinterpret_cast<double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[li];
