@@ -537,7 +537,11 @@ struct TileOffs {
 // and c+4 (6), N_a at c and c+4 (2); lane l = 4a + c.
 constexpr int LANE_TAB = 14;
 
-template <bool DET, bool ORDERED = DET>
+// Call kinds, fixed per launch so each visit body is compiled lean: matrix only, residual only, system with
+// the residual fused into the scatter (f0 = 1), system with the stress-GEMM residual (f0 != 1).
+enum { HX_MAT = 0, HX_RES = 1, HX_SYS_FUSED = 2, HX_SYS = 3 };
+
+template <bool DET, int MODE, bool ORDERED = DET>
 __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOffs& to, const HexCoef& H,
                                               const double* __restrict__ lt, double* sc, int v,
                                               unsigned char* sm) {
@@ -548,7 +552,11 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   const int HH = to.H;
   const int c = lane & 3, r = lane >> 2;
   const double* L = lt + lane * LANE_TAB;
-  const bool kd = P.values && P.rhs;  // system call: residual as K'·d (below), no stress at the points
+  // The form is linear in d: r_(a,i) = Σ_(b,m) K'_(a,i),(b,m) d_(b,m) with K' = K at f0 = 1.  With f0 = 1
+  // (static) K' is the K being written, so a system call accumulates the residual in the scatter loop
+  // (lane-local over the lane's two columns b, then over the four lanes of the row); otherwise the
+  // residual is the GEMM of the gradients with the per-point stress w σ (below).
+  constexpr bool fuse = MODE == HX_SYS_FUSED, has_rhs = MODE != HX_MAT, has_values = MODE != HX_RES;
   // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
   double C3[3][2];
 #pragma unroll
@@ -613,7 +621,7 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
 #pragma unroll
       for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
     o[9] = det;  // w (unit Gauss-Legendre weights)
-    if (!kd) {  // stress at the point for the residual-only call
+    if (has_rhs && !fuse) {  // w σ_ij at the point: B operand of the residual GEMM below
       double gu[3][3];
 #pragma unroll
       for (int k = 0; k < 3; k++)
@@ -639,19 +647,19 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   }
   const double w0 = o0[9], w1 = o1[9];
   const int li = own[a];
-  // residual-only call: the residual rows first (three registers), then the turn and the writes
+  // r_(a,i) = -Σ_γ Σ_j G_aj(γ) [w σ_ij](γ): a (8 nodes × 24) · (24 × 3) product, 6 DMMA whose A
+  // fragments are the lane's own gradients (k = point) and whose B fragments are the per-point stress
+  // rows i = lane >> 2 (zero for i >= 3); lane (a, c) receives r_(a, 2c) and r_(a, 2c + 1).
   double res[3] = {0.0, 0.0, 0.0};
-  if (P.rhs && !kd) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
+  if (has_rhs && !fuse) {
+    double r2[2] = {0.0, 0.0};
 #pragma unroll
-    for (int i = 0; i < 3; i++) {
-      double t = 0.0;
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        t = fma(o0[10 + i * 3 + j], G0[j], t);
-        t = fma(o1[10 + i * 3 + j], G1[j], t);
-      }
-      res[i] = -sum4(t);
+    for (int j = 0; j < 3; j++) {
+      dmma884(r2, G0[j], r < 3 ? o0[10 + r * 3 + j] : 0.0);
+      dmma884(r2, G1[j], r < 3 ? o1[10 + r * 3 + j] : 0.0);
     }
+    res[0] = r2[0];
+    res[1] = r2[1];
   }
   int* turn = reinterpret_cast<int*>(sm + to.turn);
   int my_turn = 0;
@@ -663,20 +671,21 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     }
     __threadfence_block();
   }
-  auto write_res = [&]() {
-    if (P.rhs && c == 0 && li >= 0) {
-      double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        if constexpr (DET) racc[i * to.T] += res[i];
-        else atomicAdd(racc + i * to.T, res[i]);
+  auto write_res = [&]() {  // GEMM residual: lane (a, c < 2) holds r_(a, 2c), r_(a, 2c + 1)
+    if (has_rhs && !fuse && c < 2 && li >= 0) {
+      double* racc = reinterpret_cast<double*>(sm + to.racc) + li + 2 * c * to.T;
+      if constexpr (DET) {
+        racc[0] -= res[0];
+        if (c == 0) racc[to.T] -= res[1];
+      } else {
+        atomicAdd(racc, -res[0]);
+        if (c == 0) atomicAdd(racc + to.T, -res[1]);
       }
     }
   };
-  if (!P.values) {
-    write_res();
-  } else {
-    double M[3][3][2];
+  // Gram blocks M^jk_ab = Σ_γ w G_aj G_bk (computed inside the turn: keeps M out of the spin loop)
+  double M[3][3][2];
+  if (has_values) {
 #pragma unroll
     for (int j = 0; j < 3; j++)
 #pragma unroll
@@ -686,23 +695,9 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
         dmma884(M[j][k], w0 * G0[j], G0[k]);
         dmma884(M[j][k], w1 * G1[j], G1[k]);
       }
-    if (kd) {  // the form is linear in d: r_(a,i) = Σ_(b,m) K'_(a,i),(b,m) d_(b,m), K' = K at f0 = 1
-      const uint16_t* hb = hv + 2 * c;
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        double t_ = 0.0;
-#pragma unroll
-        for (int t = 0; t < 2; t++) {
-          const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
-#pragma unroll
-          for (int m = 0; m < 3; m++)
-            t_ = fma(-(H.sl * M[i][m][t] + H.sm * M[m][i][t] + (i == m ? H.sm * tr : 0.0)),
-                     hdat[(3 + m) * HH + hb[t]], t_);
-        }
-        res[i] = sum4(t_);
-      }
-    }
-    write_res();
+  }
+  write_res();
+  if (has_values) {
     if (li >= 0) {
       const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li], sr = acc_row_stride(3, d, P.nnz_s);
       double* base = reinterpret_cast<double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[li];
@@ -711,21 +706,45 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       for (int t = 0; t < 2; t++) {
         const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
         double* rowb = base + lc[t];
+        double kv[9];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) kv[i * 3 + m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
         if constexpr (DET) {  // nine independent read-modify-writes: loads first (d may alias for the compiler)
-          double old[9];
 #pragma unroll
-          for (int e = 0; e < 9; e++) old[e] = rowb[(e / 3) * sr + (e % 3) * d];
+          for (int i = 0; i < 3; i++) {
+            double old[3];
 #pragma unroll
-          for (int i = 0; i < 3; i++)
+            for (int m = 0; m < 3; m++) old[m] = rowb[i * sr + m * d];
 #pragma unroll
-            for (int m = 0; m < 3; m++)
-              rowb[i * sr + m * d] = old[i * 3 + m] - (H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+            for (int m = 0; m < 3; m++) rowb[i * sr + m * d] = old[m] + kv[i * 3 + m];
+          }
         } else {
 #pragma unroll
+          for (int e = 0; e < 9; e++) atomicAdd(rowb + (e / 3) * sr + (e % 3) * d, kv[e]);
+        }
+        if constexpr (fuse) {
+          const int hb = hv[2 * c + t];
+          double dv[3];
+#pragma unroll
+          for (int m = 0; m < 3; m++) dv[m] = hdat[(3 + m) * HH + hb];
+#pragma unroll
           for (int i = 0; i < 3; i++)
 #pragma unroll
-            for (int m = 0; m < 3; m++)
-              atomicAdd(rowb + i * sr + m * d, -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0)));
+            for (int m = 0; m < 3; m++) res[i] = fma(kv[i * 3 + m], dv[m], res[i]);
+        }
+      }
+    }
+    if constexpr (fuse) {  // the four lanes of row a share li, so the group is uniform here
+#pragma unroll
+      for (int i = 0; i < 3; i++) res[i] = sum4(res[i]);
+      if (c == 0 && li >= 0) {
+        double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+          if constexpr (DET) racc[i * to.T] += res[i];
+          else atomicAdd(racc + i * to.T, res[i]);
         }
       }
     }
@@ -742,6 +761,12 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
 #endif
 constexpr int HEX_THREADS = FEM_HEX_THREADS;  // threads of the persistent hex kernel
 constexpr int HEX_WARPS = HEX_THREADS / 32;
+
+template <bool DET, int MODE>
+__device__ __forceinline__ void hex_visits(const TiledParams& P, const TileOffs& to, const HexCoef& Hc,
+                                           const double* lanetab, double* wsc, unsigned char* smem, int nv, int warp) {
+  for (int v = warp; v < nv; v += HEX_WARPS) hex_visit_el2<DET, MODE>(P, to, Hc, lanetab, wsc, v, smem);  // static split
+}
 
 template <int KH, bool DET>
 __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constant__ TiledParams P) {
@@ -778,6 +803,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
     Hc.kf0 += Fm.p[1] * Fm.f0;
     if (Fm.nu_hat >= 1) Hc.Cf1 += Fm.p[0] * Fm.f1;
   }
+  const int hmode = !P.rhs ? HX_MAT : !P.values ? HX_RES : (Hc.cl == Hc.sl && Hc.cm == Hc.sm) ? HX_SYS_FUSED : HX_SYS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const GeoFrag GF = geo_frag();
   if (warp == 0) {  // per-lane constant table (same for every warp)
@@ -854,26 +880,22 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
     __syncthreads();
     const int32_t* run = reinterpret_cast<const int32_t*>(rec + L.o_run);
     double* wsc = reinterpret_cast<double*>(F.qp) + (size_t)HEX_SCRATCH * warp;
-    if (DET && KH == 3 && !P.det_runs) {
-      // ordered: visit v takes its turn on each accumulator row it writes (vseq), so every entry sums its
+    if constexpr (KH == 3) {
+      // DET: visit v takes its turn on each accumulator row it writes (vseq), so every entry sums its
       // contributions in record order with plain adds, without block-wide barriers between colours
-      if (P.hex_dyn)  // visits are taken in increasing order, so every awaited turn belongs to a running visit
-        for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) hex_visit_el2<DET>(P, to, Hc, lanetab, wsc, v, smem);
-      else
-        for (int v = warp; v < nv; v += HEX_WARPS) hex_visit_el2<DET>(P, to, Hc, lanetab, wsc, v, smem);
+      switch (hmode) {
+        case HX_MAT: hex_visits<DET, HX_MAT>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
+        case HX_RES: hex_visits<DET, HX_RES>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
+        case HX_SYS_FUSED: hex_visits<DET, HX_SYS_FUSED>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
+        default: hex_visits<DET, HX_SYS>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
+      }
     } else if constexpr (DET) {
       for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
-        for (int v = run[r] + warp; v < run[r + 1]; v += HEX_WARPS) {
-          if constexpr (KH == 3) hex_visit_el2<true, false>(P, to, Hc, lanetab, wsc, v, smem);
-          else hex_visit<KH, true>(P, V, Hc, v);
-        }
+        for (int v = run[r] + warp; v < run[r + 1]; v += HEX_WARPS) hex_visit<KH, true>(P, V, Hc, v);
         __syncthreads();
       }
     } else {
-      for (int v = warp; v < nv; v += HEX_WARPS) {  // hex visits are uniform: static split
-        if constexpr (KH == 3) hex_visit_el2<false>(P, to, Hc, lanetab, wsc, v, smem);
-        else hex_visit<KH, false>(P, V, Hc, v);
-      }
+      for (int v = warp; v < nv; v += HEX_WARPS) hex_visit<KH, false>(P, V, Hc, v);  // uniform: static split
     }
     if (next < P.n_tiles) {  // the next record has (almost surely) landed: start its halo gather
       mbar_wait(&mbar[oth], (uint32_t)(((it + 1) >> 1) & 1));
@@ -919,8 +941,6 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
   P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
   P.spin_ns = getenv("FEM_SPIN_NS") ? atoi(getenv("FEM_SPIN_NS")) : 0;
-  P.det_runs = getenv("FEM_DET_RUNS") != nullptr;
-  P.hex_dyn = getenv("FEM_HEX_DYN") != nullptr;
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * HEX_WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
   const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + fac_bytes;
   if (smem + 4096 > 227 * 1024) {  // + static shared memory (tile offsets, lane table)

@@ -48,8 +48,6 @@ struct TiledParams {
   int acc_cap;   // doubles of the accumulator (incl. residual rows)
   int turn_cap;  // ints of the per-row turn counters (ordered deterministic kernels), multiple of 4
   int spin_ns;   // back-off of a visit waiting for its turn (FEM_SPIN_NS, default 0 = spin)
-  int det_runs;  // deterministic hex: colour runs + barriers instead of per-row turns (FEM_DET_RUNS)
-  int hex_dyn;   // hex visits taken from a shared counter instead of the static warp split (FEM_HEX_DYN)
   int fvmax;     // capacity of the facet visit arrays
 };
 

@@ -122,6 +122,25 @@ def test_genalpha_thermal_transient_term():
     S.close()
 
 
+@pytest.mark.parametrize("name", ["c5", "c3"])
+def test_genalpha_elasticity_f0(name):
+    """Gen-α factor f0 = c1 != 1 (reading L13) scales the tangent but not the residual: the hex
+    kernel cannot fuse r = K'd into the scatter and takes its stress-GEMM residual instead."""
+    _need_gpu()
+    m, p = make_config(name, "perturbed", SMALL[name])
+    p.time = TimeScheme("genalpha", 1, dt=0.05, b1=0.6, b2=0.5, c1=0.7, c2=0.8, c3=1.0)
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    assert ora["status"] == 0
+    S = _gpu_system(m, p)
+    sd = _to_dev(st)
+    for sc in SCATTERS:
+        for v, r in [S.system(sd, scatter=sc), (S.matrix(sd, scatter=sc).clone(), S.residual(sd, scatter=sc).clone())]:
+            assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL, sc
+            assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL, sc
+    S.close()
+
+
 def test_inverted_element_reported_and_edge_cases():
     _need_gpu()
     from helpers import REF_TET, one_element, problem
