@@ -661,6 +661,44 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     res[0] = r2[0];
     res[1] = r2[1];
   }
+  // K entries before taking the turn (the critical section is the read-modify-write only):
+  // M^jk_ab = Σ_γ w G_aj G_bk (18 DMMA), K_(a,i),(b,m) = -(cl M^im + cm M^mi + δ_im cm tr M) for the
+  // lane's columns b = 2c + t; with fuse, the lane's part of r = K'd as well.
+  double Kv[2][9];
+  if constexpr (has_values) {
+    double M[3][3][2];
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        M[j][k][0] = 0.0;
+        M[j][k][1] = 0.0;
+        dmma884(M[j][k], w0 * G0[j], G0[k]);
+        dmma884(M[j][k], w1 * G1[j], G1[k]);
+      }
+#pragma unroll
+    for (int t = 0; t < 2; t++) {
+      const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int m = 0; m < 3; m++) Kv[t][i * 3 + m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+    }
+    if constexpr (fuse) {
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const int hb = hv[2 * c + t];
+#pragma unroll
+        for (int m = 0; m < 3; m++) {
+          const double dv = hdat[(3 + m) * HH + hb];
+#pragma unroll
+          for (int i = 0; i < 3; i++) res[i] = fma(Kv[t][i * 3 + m], dv, res[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 3; i++) res[i] = sum4(res[i]);
+    }
+  }
   int* turn = reinterpret_cast<int*>(sm + to.turn);
   int my_turn = 0;
   if constexpr (ORDERED) {  // wait for this visit's turn on the owned row it writes (record order)
@@ -683,68 +721,37 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       }
     }
   };
-  // Gram blocks M^jk_ab = Σ_γ w G_aj G_bk (computed inside the turn: keeps M out of the spin loop)
-  double M[3][3][2];
-  if (has_values) {
-#pragma unroll
-    for (int j = 0; j < 3; j++)
-#pragma unroll
-      for (int k = 0; k < 3; k++) {
-        M[j][k][0] = 0.0;
-        M[j][k][1] = 0.0;
-        dmma884(M[j][k], w0 * G0[j], G0[k]);
-        dmma884(M[j][k], w1 * G1[j], G1[k]);
-      }
-  }
   write_res();
-  if (has_values) {
+  if constexpr (has_values) {
     if (li >= 0) {
       const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li], sr = acc_row_stride(3, d, P.nnz_s);
       double* base = reinterpret_cast<double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[li];
       const uint8_t* lc = sm + to.vloc + v * 64 + a * 8 + 2 * c;
 #pragma unroll
       for (int t = 0; t < 2; t++) {
-        const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
         double* rowb = base + lc[t];
-        double kv[9];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-          for (int m = 0; m < 3; m++) kv[i * 3 + m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
-        if constexpr (DET) {  // nine independent read-modify-writes: loads first (d may alias for the compiler)
+        if constexpr (DET) {  // independent read-modify-writes: loads first (d may alias for the compiler)
 #pragma unroll
           for (int i = 0; i < 3; i++) {
             double old[3];
 #pragma unroll
             for (int m = 0; m < 3; m++) old[m] = rowb[i * sr + m * d];
 #pragma unroll
-            for (int m = 0; m < 3; m++) rowb[i * sr + m * d] = old[m] + kv[i * 3 + m];
+            for (int m = 0; m < 3; m++) rowb[i * sr + m * d] = old[m] + Kv[t][i * 3 + m];
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 9; e++) atomicAdd(rowb + (e / 3) * sr + (e % 3) * d, kv[e]);
-        }
-        if constexpr (fuse) {
-          const int hb = hv[2 * c + t];
-          double dv[3];
-#pragma unroll
-          for (int m = 0; m < 3; m++) dv[m] = hdat[(3 + m) * HH + hb];
-#pragma unroll
-          for (int i = 0; i < 3; i++)
-#pragma unroll
-            for (int m = 0; m < 3; m++) res[i] = fma(kv[i * 3 + m], dv[m], res[i]);
+          for (int e = 0; e < 9; e++) atomicAdd(rowb + (e / 3) * sr + (e % 3) * d, Kv[t][e]);
         }
       }
-    }
-    if constexpr (fuse) {  // the four lanes of row a share li, so the group is uniform here
+      if constexpr (fuse) {
+        if (c == 0) {
+          double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
 #pragma unroll
-      for (int i = 0; i < 3; i++) res[i] = sum4(res[i]);
-      if (c == 0 && li >= 0) {
-        double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
-#pragma unroll
-        for (int i = 0; i < 3; i++) {
-          if constexpr (DET) racc[i * to.T] += res[i];
-          else atomicAdd(racc + i * to.T, res[i]);
+          for (int i = 0; i < 3; i++) {
+            if constexpr (DET) racc[i * to.T] += res[i];
+            else atomicAdd(racc + i * to.T, res[i]);
+          }
         }
       }
     }

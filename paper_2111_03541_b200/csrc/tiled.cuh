@@ -569,19 +569,18 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 
 // Write every owned row once and the residual rows.  A row segment whose shared-memory copy has the
 // 16-byte phase of its destination (the record layout arranges it, see acc_row_stride) leaves by one
-// bulk store of its aligned middle plus at most two single doubles; other rows are copied by a warp.
-// The bulk stores drain to HBM asynchronously; only their shared-memory reads are awaited (before the
-// accumulator is reused).
+// bulk store of its aligned middle plus at most two single doubles; other rows are copied element by
+// element.  One thread per row (a tile has a few hundred rows): the bulk stores drain to HBM
+// asynchronously; only their shared-memory reads are awaited (before the accumulator is reused).
 template <int KH>
 __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const TileSmem& S) {
   fence_proxy_async_smem();  // generic-proxy accumulator writes -> async-proxy (bulk copy) reads
   __syncthreads();
-  const int tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, T = S.T;
-  const int lane = tid & 31, nw = nth >> 5;
+  const int tid = threadIdx.x, nth = blockDim.x, T = S.T;
   if (P.values) {
     bool issued = false;
-    for (int rr = warp; rr < T * KH; rr += nw) {
-      const int li = rr / KH, k0 = rr % KH;
+    for (int rr = tid; rr < T * KH; rr += nth) {
+      const int li = rr / KH, k0 = rr - li * KH;
       const int d = S.tdeg[li];
       const int len = KH * d;
       const double* src = S.acc + S.toff[li] + k0 * acc_row_stride(KH, d, P.nnz_s);
@@ -589,14 +588,12 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const TileSm
       if ((((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0 && len >= 4) {
         const int head = ((uintptr_t)dst & 15) ? 1 : 0;
         const int mid = (len - head) & ~1;
-        if (lane == 0) {
-          bulk_s2g(dst + head, src + head, 8u * (uint32_t)mid);
-          issued = true;
-        }
-        if (lane == 1 && head) dst[0] = src[0];
-        if (lane == 2 && head + mid < len) dst[len - 1] = src[len - 1];
+        bulk_s2g(dst + head, src + head, 8u * (uint32_t)mid);
+        issued = true;
+        if (head) dst[0] = src[0];
+        if (head + mid < len) dst[len - 1] = src[len - 1];
       } else {
-        for (int j = lane; j < len; j += 32) dst[j] = src[j];
+        for (int j = 0; j < len; j++) dst[j] = src[j];
       }
     }
     if (issued) {
