@@ -345,7 +345,10 @@ static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
 }
 
 constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
-constexpr int HEX_SCRATCH = 160; // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
+constexpr int HEX_SCRATCH = 176; // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
+// Row r of the geometry GEMM output in the warp scratch: 24 r + (r >> 1), so the 4 x 4 lanes of a
+// half-warp storing their accumulator fragments hit 16 distinct bank pairs.
+__device__ __forceinline__ constexpr int hx_goff(int r) { return 24 * r + (r >> 1); }
 
 // Reference-gradient B fragments of the geometry GEMM (constant per lane): for k-step s and n-tile t,
 // lane l holds ∇̂N_a(ξ_q)_j with a = 4s + (l&3), (q, j) = divmod(8t + (l>>2), 3).
@@ -551,12 +554,15 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   const double* hdat = reinterpret_cast<const double*>(sm + to.hdat);
   const int HH = to.H;
   const int c = lane & 3, r = lane >> 2;
-  const double* L = lt + lane * LANE_TAB;
+  const double* L = lt + lane;  // lane table, transposed: L[32 k] = constant k of this lane
   // The form is linear in d: r_(a,i) = Σ_(b,m) K'_(a,i),(b,m) d_(b,m) with K' = K at f0 = 1.  With f0 = 1
   // (static) K' is the K being written, so a system call accumulates the residual in the scatter loop
   // (lane-local over the lane's two columns b, then over the four lanes of the row); otherwise the
   // residual is the GEMM of the gradients with the per-point stress w σ (below).
   constexpr bool fuse = MODE == HX_SYS_FUSED, has_rhs = MODE != HX_MAT, has_values = MODE != HX_RES;
+  // per-point record stride (doubles): J^-1, w [, w σ]; even (16-byte loads) and ≡ 2·odd mod 16, so the
+  // eight writer lanes (one per point) hit distinct bank pairs
+  constexpr int RS = (has_rhs && !fuse) ? 22 : 10;
   // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
   double C3[3][2];
 #pragma unroll
@@ -565,13 +571,13 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   for (int s = 0; s < 2; s++) {
     const double av = r < 6 ? hdat[r * HH + hv[4 * s + c]] : 0.0;
 #pragma unroll
-    for (int t = 0; t < 3; t++) dmma884(C3[t], av, L[s * 3 + t]);
+    for (int t = 0; t < 3; t++) dmma884(C3[t], av, L[32 * (s * 3 + t)]);
   }
   if (r < 6) {
 #pragma unroll
     for (int t = 0; t < 3; t++) {
-      sc[r * 24 + 8 * t + 2 * c] = C3[t][0];
-      sc[r * 24 + 8 * t + 2 * c + 1] = C3[t][1];
+      sc[hx_goff(r) + 8 * t + 2 * c] = C3[t][0];
+      sc[hx_goff(r) + 8 * t + 2 * c + 1] = C3[t][1];
     }
   }
   __syncwarp();
@@ -581,8 +587,8 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   for (int i = 0; i < 3; i++)
 #pragma unroll
     for (int j = 0; j < 3; j++) {
-      J[i][j] = sc[i * 24 + 3 * q + j];
-      Dr[i][j] = sc[(3 + i) * 24 + 3 * q + j];
+      J[i][j] = sc[hx_goff(i) + 3 * q + j];
+      Dr[i][j] = sc[hx_goff(3 + i) + 3 * q + j];
     }
   const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
   const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
@@ -615,7 +621,7 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
     Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
     Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
-    double* o = sc + q * 20;  // per-point records (the GEMM output has been consumed)
+    double* o = sc + q * RS;  // per-point records (the GEMM output has been consumed)
 #pragma unroll
     for (int j = 0; j < 3; j++)
 #pragma unroll
@@ -637,15 +643,22 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   __syncwarp();
   // ---- fragment layout: node a = lane >> 2, points c and c + 4
   const int a = r;
-  const double* o0 = sc + c * 20;
-  const double* o1 = sc + (c + 4) * 20;
+  const double* o0 = sc + c * RS;
+  const double* o1 = sc + (c + 4) * RS;
+  double R0[10], R1[10];  // J^-1 (9) and w of points c and c + 4: 16-byte loads of broadcast records
+#pragma unroll
+  for (int k = 0; k < 5; k++) {
+    const double2 x0 = reinterpret_cast<const double2*>(o0)[k], x1 = reinterpret_cast<const double2*>(o1)[k];
+    R0[2 * k] = x0.x; R0[2 * k + 1] = x0.y;
+    R1[2 * k] = x1.x; R1[2 * k + 1] = x1.y;
+  }
   double G0[3], G1[3];
 #pragma unroll
   for (int i = 0; i < 3; i++) {
-    G0[i] = o0[0 * 3 + i] * L[6] + o0[1 * 3 + i] * L[7] + o0[2 * 3 + i] * L[8];
-    G1[i] = o1[0 * 3 + i] * L[9] + o1[1 * 3 + i] * L[10] + o1[2 * 3 + i] * L[11];
+    G0[i] = R0[0 * 3 + i] * L[32 * 6] + R0[1 * 3 + i] * L[32 * 7] + R0[2 * 3 + i] * L[32 * 8];
+    G1[i] = R1[0 * 3 + i] * L[32 * 9] + R1[1 * 3 + i] * L[32 * 10] + R1[2 * 3 + i] * L[32 * 11];
   }
-  const double w0 = o0[9], w1 = o1[9];
+  const double w0 = R0[9], w1 = R1[9];
   const int li = own[a];
   // r_(a,i) = -Σ_γ Σ_j G_aj(γ) [w σ_ij](γ): a (8 nodes × 24) · (24 × 3) product, 6 DMMA whose A
   // fragments are the lane's own gradients (k = point) and whose B fragments are the per-point stress
@@ -814,17 +827,17 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
   const int tid = threadIdx.x, warp = tid >> 5;
   const GeoFrag GF = geo_frag();
   if (warp == 0) {  // per-lane constant table (same for every warp)
-    double* Lt = lanetab + tid * LANE_TAB;
+    double* Lt = lanetab + tid;  // transposed (constant k of lane l at 32 k + l): conflict-free loads
 #pragma unroll
     for (int s = 0; s < 2; s++)
 #pragma unroll
-      for (int t = 0; t < 3; t++) Lt[s * 3 + t] = GF.b[s][t];
+      for (int t = 0; t < 3; t++) Lt[32 * (s * 3 + t)] = GF.b[s][t];
     double g0[3], g1[3], N0, N1;
     hex_ref(tid >> 2, tid & 3, g0, N0);
     hex_ref(tid >> 2, (tid & 3) + 4, g1, N1);
-    for (int i = 0; i < 3; i++) { Lt[6 + i] = g0[i]; Lt[9 + i] = g1[i]; }
-    Lt[12] = N0;
-    Lt[13] = N1;
+    for (int i = 0; i < 3; i++) { Lt[32 * (6 + i)] = g0[i]; Lt[32 * (9 + i)] = g1[i]; }
+    Lt[32 * 12] = N0;
+    Lt[32 * 13] = N1;
   }
   int64_t tile = blockIdx.x;
   if (tile >= P.n_tiles) return;
