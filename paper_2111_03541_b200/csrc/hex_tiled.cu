@@ -345,7 +345,9 @@ static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
 }
 
 constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
-constexpr int HEX_SCRATCH = 176; // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
+constexpr int HEX_SCRATCH = 200;  // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
+// exchanged gradient G_a,i(ξ_q) in the warp scratch: [i][q][a], a swizzled by bit 1 of q; w at 192 + q
+__device__ __forceinline__ constexpr int hx_gx(int i, int q, int a) { return 64 * i + 8 * q + (a ^ (4 * ((q >> 1) & 1))); }
 // Row r of the geometry GEMM output in the warp scratch: 24 r + (r >> 1), so the 4 x 4 lanes of a
 // half-warp storing their accumulator fragments hit 16 distinct bank pairs.
 __device__ __forceinline__ constexpr int hx_goff(int r) { return 24 * r + (r >> 1); }
@@ -537,8 +539,8 @@ struct TileOffs {
   int H, T;
 };
 // Per-lane constants of the fragment layout: B fragments of the geometry GEMM (6), ∇̂N_a at points c
-// and c+4 (6), N_a at c and c+4 (2); lane l = 4a + c.
-constexpr int LANE_TAB = 14;
+// and c+4 (6) for lane l = 4a + c; ∇̂N_c and ∇̂N_(c+4) at point q (6) for l = 4q + c.
+constexpr int LANE_TAB = 18;
 
 // Call kinds, fixed per launch so each visit body is compiled lean: matrix only, residual only, system with
 // the residual fused into the scatter (f0 = 1), system with the stress-GEMM residual (f0 != 1).
@@ -560,9 +562,10 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   // (lane-local over the lane's two columns b, then over the four lanes of the row); otherwise the
   // residual is the GEMM of the gradients with the per-point stress w σ (below).
   constexpr bool fuse = MODE == HX_SYS_FUSED, has_rhs = MODE != HX_MAT, has_values = MODE != HX_RES;
-  // per-point record stride (doubles): J^-1, w [, w σ]; even (16-byte loads) and ≡ 2·odd mod 16, so the
-  // eight writer lanes (one per point) hit distinct bank pairs
-  constexpr int RS = (has_rhs && !fuse) ? 22 : 10;
+  // stress mode: per-point record stride (doubles) J^-1, w, w σ; even (16-byte loads) and ≡ 2·odd mod 16,
+  // so the eight writer lanes (one per point) hit distinct bank pairs
+  constexpr bool stress = has_rhs && !fuse;  // residual from the per-point stress (residual-only, f0 != 1)
+  constexpr int RS = 22;
   // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
   double C3[3][2];
 #pragma unroll
@@ -611,23 +614,44 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     return;
   }
   __syncwarp();  // everyone has read the GEMM output; the scratch now takes the per-point records
-  if (c == 0) {
-    const double rr = 1.0 / det;
-    double Ji[3][3];
-    Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
-    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
-    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
-    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
-    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
-    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
-    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
-    double* o = sc + q * RS;  // per-point records (the GEMM output has been consumed)
+  const double rr = 1.0 / det;
+  double Ji[3][3];  // Ji[j][i] = (J^-1)_ji, in every lane of point group q
+  Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+  const int a = r;
+  double G0[3], G1[3], w0, w1;
+  if constexpr (!stress) {
+    // gradient exchange: lane (q, c) forms G_a(q) = J^-T ∇̂N_a(ξ_q) for a = c, c + 4 and stores it at
+    // [i][q][a ^ 4((q >> 1) & 1)] (the swizzle makes stores and loads conflict-free); lane (a, c) then
+    // loads G_a at its points c and c + 4 — the A/B fragment layout of the Gram GEMM
 #pragma unroll
-    for (int j = 0; j < 3; j++)
+    for (int h = 0; h < 2; h++)
 #pragma unroll
-      for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
-    o[9] = det;  // w (unit Gauss-Legendre weights)
-    if (has_rhs && !fuse) {  // w σ_ij at the point: B operand of the residual GEMM below
+      for (int i = 0; i < 3; i++)
+        sc[hx_gx(i, q, c + 4 * h)] = Ji[0][i] * L[32 * (12 + 3 * h)] + Ji[1][i] * L[32 * (13 + 3 * h)] + Ji[2][i] * L[32 * (14 + 3 * h)];
+    if (c == 0) sc[192 + q] = det;  // w (unit Gauss-Legendre weights)
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      G0[i] = sc[hx_gx(i, c, a)];
+      G1[i] = sc[hx_gx(i, c + 4, a)];
+    }
+    w0 = sc[192 + c];
+    w1 = sc[196 + c];
+  } else {
+    if (c == 0) {
+      double* o = sc + q * RS;  // per-point records (the GEMM output has been consumed)
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
+      o[9] = det;  // w (unit Gauss-Legendre weights)
+      // w σ_ij at the point: B operand of the residual GEMM below
       double gu[3][3];
 #pragma unroll
       for (int k = 0; k < 3; k++)
@@ -639,32 +663,33 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
 #pragma unroll
         for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
     }
-  }
-  __syncwarp();
-  // ---- fragment layout: node a = lane >> 2, points c and c + 4
-  const int a = r;
-  const double* o0 = sc + c * RS;
-  const double* o1 = sc + (c + 4) * RS;
-  double R0[10], R1[10];  // J^-1 (9) and w of points c and c + 4: 16-byte loads of broadcast records
+    __syncwarp();
+    // ---- fragment layout: node a = lane >> 2, points c and c + 4
+    const double* o0 = sc + c * RS;
+    const double* o1 = sc + (c + 4) * RS;
+    double R0[10], R1[10];  // J^-1 (9) and w of points c and c + 4: 16-byte loads of broadcast records
 #pragma unroll
-  for (int k = 0; k < 5; k++) {
-    const double2 x0 = reinterpret_cast<const double2*>(o0)[k], x1 = reinterpret_cast<const double2*>(o1)[k];
-    R0[2 * k] = x0.x; R0[2 * k + 1] = x0.y;
-    R1[2 * k] = x1.x; R1[2 * k + 1] = x1.y;
-  }
-  double G0[3], G1[3];
+    for (int k = 0; k < 5; k++) {
+      const double2 x0 = reinterpret_cast<const double2*>(o0)[k], x1 = reinterpret_cast<const double2*>(o1)[k];
+      R0[2 * k] = x0.x; R0[2 * k + 1] = x0.y;
+      R1[2 * k] = x1.x; R1[2 * k + 1] = x1.y;
+    }
 #pragma unroll
-  for (int i = 0; i < 3; i++) {
-    G0[i] = R0[0 * 3 + i] * L[32 * 6] + R0[1 * 3 + i] * L[32 * 7] + R0[2 * 3 + i] * L[32 * 8];
-    G1[i] = R1[0 * 3 + i] * L[32 * 9] + R1[1 * 3 + i] * L[32 * 10] + R1[2 * 3 + i] * L[32 * 11];
+    for (int i = 0; i < 3; i++) {
+      G0[i] = R0[0 * 3 + i] * L[32 * 6] + R0[1 * 3 + i] * L[32 * 7] + R0[2 * 3 + i] * L[32 * 8];
+      G1[i] = R1[0 * 3 + i] * L[32 * 9] + R1[1 * 3 + i] * L[32 * 10] + R1[2 * 3 + i] * L[32 * 11];
+    }
+    w0 = R0[9];
+    w1 = R1[9];
   }
-  const double w0 = R0[9], w1 = R1[9];
   const int li = own[a];
   // r_(a,i) = -Σ_γ Σ_j G_aj(γ) [w σ_ij](γ): a (8 nodes × 24) · (24 × 3) product, 6 DMMA whose A
   // fragments are the lane's own gradients (k = point) and whose B fragments are the per-point stress
   // rows i = lane >> 2 (zero for i >= 3); lane (a, c) receives r_(a, 2c) and r_(a, 2c + 1).
   double res[3] = {0.0, 0.0, 0.0};
-  if (has_rhs && !fuse) {
+  if constexpr (stress) {
+    const double* o0 = sc + c * RS;
+    const double* o1 = sc + (c + 4) * RS;
     double r2[2] = {0.0, 0.0};
 #pragma unroll
     for (int j = 0; j < 3; j++) {
@@ -836,8 +861,10 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
     hex_ref(tid >> 2, tid & 3, g0, N0);
     hex_ref(tid >> 2, (tid & 3) + 4, g1, N1);
     for (int i = 0; i < 3; i++) { Lt[32 * (6 + i)] = g0[i]; Lt[32 * (9 + i)] = g1[i]; }
-    Lt[32 * 12] = N0;
-    Lt[32 * 13] = N1;
+    double gc[3], gc4[3], Nc, Nc4;  // writer role of the gradient exchange: lane 4q + c, nodes c and c + 4 at point q
+    hex_ref(tid & 3, tid >> 2, gc, Nc);
+    hex_ref((tid & 3) + 4, tid >> 2, gc4, Nc4);
+    for (int i = 0; i < 3; i++) { Lt[32 * (12 + i)] = gc[i]; Lt[32 * (15 + i)] = gc4[i]; }
   }
   int64_t tile = blockIdx.x;
   if (tile >= P.n_tiles) return;
@@ -963,8 +990,11 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.spin_ns = getenv("FEM_SPIN_NS") ? atoi(getenv("FEM_SPIN_NS")) : 0;
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * HEX_WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
   const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + fac_bytes;
-  if (smem + 4096 > 227 * 1024) {  // + static shared memory (tile offsets, lane table)
-    set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
+  cudaFuncAttributes fa;
+  FEM_CUDA_TRY(cudaFuncGetAttributes(&fa, k_hex_rec<KH, DET>));
+  if (smem + fa.sharedSizeBytes > 227 * 1024) {  // + static shared memory (tile offsets, lane table)
+    set_error("hex record kernel: shared memory request too large (" + std::to_string(smem) + " B dynamic + " +
+              std::to_string(fa.sharedSizeBytes) + " B static)");
     return FEM_E_UNSUPPORTED;
   }
   FEM_CUDA_TRY(cudaFuncSetAttribute(k_hex_rec<KH, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
