@@ -60,6 +60,7 @@ struct TileSchedule {
   uint8_t* rec = nullptr;        // device: packed per-tile records (layout rec_layout)
   int64_t* rec_off = nullptr;    // device [n_tiles+1] byte offsets
   int64_t rec_max = 0, rec_bytes_total = 0;
+  int max_turns = 0;              // most visits of one tile touching one owned point (ordered kernels need <= 255)
 };
 
 // Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by

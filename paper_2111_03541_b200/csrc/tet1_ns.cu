@@ -6,8 +6,10 @@
 // Rm_i(γ) = ρ u_k(γ) u_i,k + p_,i is linear in u(γ) (u_i,kk = 0, reading L10).  A warp takes two
 // element visits at once: lane (h, a, b) with h = lane>>4 computes the geometry of visit h and the
 // 4x4 block of the pair (a, b) summed over the 4 points; the same lanes then take the residual rows
-// (a, κ0).  Contributions go to the tile accumulator with shared-memory fp64 atomics.  Boundary
-// groups (inflow/outflow/fix) reuse the generic warp path.
+// (a, κ0).  Contributions go to the tile accumulator with shared-memory fp64 atomics (CAS loops on
+// sm_100), or, with FEM_NS_DET, with plain read-modify-writes in record order (per-row turns,
+// bit-identical run to run, ~25% slower on c4).  Boundary groups (inflow/outflow/fix) reuse the generic
+// warp path.
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -23,8 +25,9 @@ struct NsCoef {
 // Per-visit point data in the warp scratch (doubles): G[4][3] | gu[4][3] | Rc | w | u[4 points][4] | Rm[4][3]
 constexpr int NS_SC = 12 + 12 + 2 + 16 + 12;  // 54 doubles per visit
 
+template <bool DET>
 __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& D, const NsCoef& c, int v0, int nv,
-                                          double* scw) {
+                                          double* scw, const uint8_t* vseq, int* turn) {
   const int lane = threadIdx.x & 31;
   const int h = lane >> 4, l16 = lane & 15;
   const int v = v0 + h;
@@ -32,17 +35,16 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
   const int vv = valid ? v : v0;
   const double al = 0.13819660112501051518, be = 0.58541019662496845446;  // (5-√5)/20, (5+3√5)/20
   double* sc = scw + h * NS_SC;
-  // ---- phase 1: lane 0 of each half-warp computes the visit's constants (affine P1 tet)
+  // ---- phase 1: the 16 lanes of each half-warp compute the visit's constants (affine P1 tet): the
+  // geometry redundantly (SIMT: same issue cost as one lane), the per-lane values split over the lanes
   bool bad = false;
-  if (l16 == 0) {
-    double X[4][3], U[4][4];
+  {
+    double X[4][3];
 #pragma unroll
     for (int n = 0; n < 4; n++) {
       const int hh = (uint16_t)D.vhal[vv * 4 + n];
 #pragma unroll
       for (int d = 0; d < 3; d++) X[n][d] = D.hdat[d * D.H + hh];
-#pragma unroll
-      for (int k = 0; k < 4; k++) U[k][n] = D.hdat[(3 + k) * D.H + hh];
     }
     double J[3][3];
 #pragma unroll
@@ -71,35 +73,59 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
       G[3][i] = Ji[2][i];
       G[0][i] = -(Ji[0][i] + Ji[1][i] + Ji[2][i]);
     }
+    // lane l16 < 12: G[n][i] and gu[k][i] = u_k,i = Σ_n U[k][n] G[n][i] for (k, i) = (l16 / 3, l16 % 3);
+    // every lane: u_k(γ) for (γ, k) = (l16 / 4, l16 % 4)
+    if (l16 < 12) {
+      const int k = l16 / 3, i = l16 % 3;
+      double g = 0.0;
 #pragma unroll
-    for (int n = 0; n < 4; n++)
-#pragma unroll
-      for (int i = 0; i < 3; i++) sc[n * 3 + i] = G[n][i];
-    double gu[4][3];
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        gu[k][i] = U[k][0] * G[0][i] + U[k][1] * G[1][i] + U[k][2] * G[2][i] + U[k][3] * G[3][i];
-        sc[12 + k * 3 + i] = gu[k][i];
+      for (int n = 0; n < 4; n++) {
+        const int hh = (uint16_t)D.vhal[vv * 4 + n];
+        g = fma(D.hdat[(3 + k) * D.H + hh], G[n][i], g);
       }
-    sc[24] = gu[0][0] + gu[1][1] + gu[2][2];  // Rc
-    sc[25] = det * (1.0 / 24.0);                // w (4-point rule weight 1/24)
+      sc[12 + l16] = g;
+      double gsel = G[0][0];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      double u[4];
+      for (int n = 0; n < 4; n++)
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        u[k] = al * (U[k][0] + U[k][1] + U[k][2] + U[k][3]) + (be - al) * U[k][q];
-        sc[26 + q * 4 + k] = u[k];
+        for (int ii = 0; ii < 3; ii++)
+          if (n * 3 + ii == l16) gsel = G[n][ii];
+      sc[l16] = gsel;
+    }
+    {
+      const int q = l16 >> 2, k = l16 & 3;
+      double us = 0.0, uq = 0.0;
+#pragma unroll
+      for (int n = 0; n < 4; n++) {
+        const int hh = (uint16_t)D.vhal[vv * 4 + n];
+        const double U = D.hdat[(3 + k) * D.H + hh];
+        us += U;
+        if (n == q) uq = U;
       }
-#pragma unroll
-      for (int i = 0; i < 3; i++)  // Rm_i = ρ u_k u_i,k + p_,i
-        sc[42 + q * 3 + i] = gu[3][i] + c.rho * (u[0] * gu[i][0] + u[1] * gu[i][1] + u[2] * gu[i][2]);
+      sc[26 + q * 4 + k] = al * us + (be - al) * uq;
+    }
+    if (l16 == 0) sc[25] = det * (1.0 / 24.0);  // w (4-point rule weight 1/24)
+    __syncwarp();
+    if (l16 == 12) sc[24] = sc[12 + 0] + sc[12 + 4] + sc[12 + 8];  // Rc = u_k,k
+    if (l16 < 12) {  // Rm_i(γ) = ρ u_k(γ) u_i,k + p_,i for (γ, i) = (l16 / 3, l16 % 3)
+      const int q = l16 / 3, i = l16 % 3;
+      const double* u = sc + 26 + q * 4;
+      sc[42 + q * 3 + i] = sc[12 + 9 + i] + c.rho * (u[0] * sc[12 + i * 3 + 0] + u[1] * sc[12 + i * 3 + 1] + u[2] * sc[12 + i * 3 + 2]);
     }
   }
   if (__any_sync(0xffffffffu, bad)) {
     if (bad) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)D.vid[v]);
+    if constexpr (DET) {  // still pass the turns on, or later visits of these rows would wait forever
+      const int a = l16 >> 2, li = D.vown[vv * 4 + a];
+      if (valid && li >= 0 && (l16 & 3) == 0) {
+        volatile int* tp = turn + li;
+        const int t = vseq[vv * 4 + a];
+        while (*tp != t) {
+        }
+        __threadfence_block();
+        *tp = t + 1;
+      }
+    }
     __syncwarp();
     return;
   }
@@ -157,7 +183,36 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
       res += w * (Na * Rc + tm * (Ga[0] * Rm[0] + Ga[1] * Rm[1] + Ga[2] * Rm[2]));
     }
   }
-  if (valid && li >= 0) {
+  if constexpr (DET) {
+    // ordered: visit v takes its turn (vseq) on the accumulator row of each owned node, so every entry
+    // sums its contributions in record order with plain read-modify-writes (bit-identical run to run).
+    // Visits are grabbed in increasing order, so an awaited turn belongs to a running visit (possibly
+    // the other half of this warp, which independent thread scheduling lets finish).
+    const unsigned half = 0xffffu << (16 * h);
+    int my_turn = 0;
+    if (valid && li >= 0) {
+      my_turn = vseq[vv * 4 + a];
+      while (*reinterpret_cast<volatile int*>(turn + li) != my_turn) {
+      }
+      __threadfence_block();
+      if (P.values) {
+        const int d = D.tdeg[li], sr = acc_row_stride(4, d, P.nnz_s);
+        double* rowb = D.acc + D.toff[li] + D.vloc[vv * 16 + a * 4 + b];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          double old[4];
+#pragma unroll
+          for (int m = 0; m < 4; m++) old[m] = rowb[i * sr + m * d];
+#pragma unroll
+          for (int m = 0; m < 4; m++) rowb[i * sr + m * d] = fma(c.f0, acc[i][m], old[m]);
+        }
+      }
+      if (P.rhs) D.racc[b * D.T + li] += res;
+    }
+    __syncwarp(half);  // the row's four lanes have written
+    __threadfence_block();
+    if (valid && li >= 0 && b == 0) *reinterpret_cast<volatile int*>(turn + li) = my_turn + 1;
+  } else if (valid && li >= 0) {
     if (P.values) {
       const int d = D.tdeg[li], sr = acc_row_stride(4, d, P.nnz_s);
       double* rowb = D.acc + D.toff[li] + D.vloc[vv * 16 + a * 4 + b];
@@ -171,7 +226,7 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
   __syncwarp();  // scratch reused by the next pair of visits
 }
 
-template <bool PAD>
+template <bool DET>
 __global__ void __launch_bounds__(TILED_THREADS, 1) k_ns_rec(const __grid_constant__ TiledParams P) {
   using C = TileCfg<ET_TET, 1, 4, 2>;
   constexpr int NL = 4, DIM = 3;
@@ -182,7 +237,8 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_ns_rec(const __grid_consta
   double* hbuf = reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap);
   double* acc = hbuf + P.hcap;
   TileSmem S;
-  unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
+  int* turn = reinterpret_cast<int*>(acc + P.acc_cap);
+  unsigned char* fp = reinterpret_cast<unsigned char*>(turn + P.turn_cap);
   S.qp = fp;
   fp += std::max((size_t)P.rec_bytes * 8, (size_t)8 * 2 * NS_SC * C::WARPS);
   S.vid = reinterpret_cast<int32_t*>(fp);
@@ -254,19 +310,22 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_ns_rec(const __grid_consta
     D.racc = acc + acc_n;
     D.T = T;
     for (int i = tid; i < acc_n + 4 * T; i += blockDim.x) acc[i] = 0.0;
+    if constexpr (DET)
+      for (int i = tid; i < T; i += blockDim.x) turn[i] = 0;
     if (tid == 0) *ctr = 0;
     cp_async_wait_all();
     __syncthreads();
     double* scw = reinterpret_cast<double*>(S.qp) + (size_t)2 * NS_SC * warp;
-    for (int v0 = grab_visits(ctr, 2); v0 < nv; v0 = grab_visits(ctr, 2)) ns_visit2(P, D, cf, v0, nv, scw);
-    if (fmask) rec_facets<ET_TET, 1, 4, 2, 8>(P, D, rec, L, slot);
+    const uint8_t* vseq = rec + L.o_vseq;
+    for (int v0 = grab_visits(ctr, 2); v0 < nv; v0 = grab_visits(ctr, 2)) ns_visit2<DET>(P, D, cf, v0, nv, scw, vseq, turn);
+    if (fmask) rec_facets<ET_TET, 1, 4, 2, 8, DET>(P, D, rec, L, slot);
     tile_epilogue<4>(P, D);
     __syncthreads();
   }
 }
 
 // NS on P1 tets, 4-point rule, exactly one domain term NS_DOMAIN.
-int launch_ns_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled) {
+int launch_ns_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_t s, bool* handled) {
   *handled = false;
   if (P.n_dom != 1 || P.dom[0].form != FEM_WF_NS_DOMAIN || !T.rec) return 0;
   *handled = true;
@@ -286,19 +345,22 @@ int launch_ns_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool*
   P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
   P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)4 * T.max_tile_nodes);
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
+  P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * 8, (size_t)8 * 2 * NS_SC * C::WARPS) + (size_t)fv * (4 + NL * 6 + 1) + 16;
-  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
+  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + fac_bytes;
   if (smem > 227 * 1024) {
     set_error("NS record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
     return FEM_E_UNSUPPORTED;
   }
-  FEM_CUDA_TRY(cudaFuncSetAttribute(k_ns_rec<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (det) FEM_CUDA_TRY(cudaFuncSetAttribute(k_ns_rec<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  else FEM_CUDA_TRY(cudaFuncSetAttribute(k_ns_rec<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (T.n_tiles <= 0) return 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
-  k_ns_rec<false><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  if (det) k_ns_rec<true><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  else k_ns_rec<false><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -477,6 +477,7 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     }
     std::vector<uint8_t> buf((size_t)roff[n_tiles], 0);
     std::vector<int64_t> vis_loc(dom_items.size());
+    int max_turns_all = 0;
     for (int64_t t = 0; t < n_tiles; t++) {
       const int Tn = (int)(tile_off[t + 1] - tile_off[t]);
       const int H = (int)(hoff[t + 1] - hoff[t]);
@@ -535,7 +536,9 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
         }
         vis_loc[gi] = roff[t] + L.o_vloc + (int64_t)v * NL * NL;
       }
+      for (int i = 0; i < Tn; i++) max_turns_all = std::max(max_turns_all, turn[i]);
     }
+    T.max_turns = max_turns_all;
     FEM_CUDA_TRY(cudaMalloc(&T.rec, buf.size() + 16));
     FEM_CUDA_TRY(cudaMalloc(&T.rec_off, sizeof(int64_t) * (n_tiles + 1)));
     FEM_CUDA_TRY(cudaMemcpy(T.rec, buf.data(), buf.size(), cudaMemcpyHostToDevice));
@@ -785,15 +788,19 @@ int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_proble
   P.values = values; P.rhs = rhs; P.err = m->err;
   P.nu_hat = prob->time.kind == FEM_TIME_GENALPHA ? prob->time.nu_hat : 0;
   const int et = m->etype, o = m->order, kh = m->kh, q = prob->quad_order;
+  // ordered (bit-identical run to run) unless FEM_TILED_NONDET asks for the atomic variant; per-row turn
+  // numbers are bytes, so a tile point touched by more than 256 visits takes the atomic variant
+  const bool det = getenv("FEM_TILED_NONDET") == nullptr && T.max_turns <= 256;
   if (et == ET_HEX && o == 1 && q == 2 && !getenv("FEM_NO_HEX_MMA")) {
     bool handled = false;
-    // colour-synchronous (bit-exact run to run) unless FEM_TILED_NONDET asks for the atomic variant
-    const int rc = launch_hex_tiled(P, T, kh, getenv("FEM_TILED_NONDET") == nullptr, s, &handled);
+    const int rc = launch_hex_tiled(P, T, kh, det, s, &handled);
     if (handled) return rc;
   }
   if (et == ET_TET && o == 1 && kh == 4 && q == 2 && !getenv("FEM_NO_NS_SPEC")) {
     bool handled = false;
-    const int rc = launch_ns_tiled(P, T, s, &handled);
+    // ordered turns cost ~25% on tets (24 elements per vertex: consecutive visits share rows), so the
+    // NS kernel is ordered only on request (FEM_NS_DET); the coloured scatter is deterministic too
+    const int rc = launch_ns_tiled(P, T, det && getenv("FEM_NS_DET") != nullptr, s, &handled);
     if (handled) return rc;
   }
   if (et == ET_TET && o == 2 && kh == 3 && q == 2 && !getenv("FEM_NO_P2_SPEC")) {

@@ -636,7 +636,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled);
-int launch_ns_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled);
+int launch_ns_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_t s, bool* handled);
 int launch_p2_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled);
 
 }  // namespace fem

@@ -75,17 +75,22 @@ def test_small_parity_all_modes(name, variant):
 
 
 @pytest.mark.parametrize("name,sc", [(n, "coloured") for n in ("c2", "c3", "c4", "c5")] +
-                         [("c2", "tiled"), ("c5", "tiled")])
+                         [("c2", "tiled"), ("c5", "tiled"), ("c4", "tiled")])
 def test_deterministic_modes_bit_exact(name, sc):
-    """Coloured scatter everywhere, and the tiled path on Q1 hex (colour-synchronous visits)."""
+    """Coloured scatter everywhere, and the tiled path on Q1 hex and (FEM_NS_DET) P1 NS tets (per-row
+    turns: every accumulator entry sums its contributions in record order)."""
     _need_gpu()
     m, p = make_config(name, "perturbed", SMALL[name])
     st = _to_dev(make_state(name, m, p))
     S = _gpu_system(m, p)
-    ref_v, ref_r = [x.clone() for x in S.system(st, scatter=sc)]
-    for _ in range(3):
-        v, r = S.system(st, scatter=sc)
-        assert torch.equal(v, ref_v) and torch.equal(r, ref_r)
+    os.environ["FEM_NS_DET"] = "1"  # read at launch: the NS tile kernel's ordered variant is opt-in
+    try:
+        ref_v, ref_r = [x.clone() for x in S.system(st, scatter=sc)]
+        for _ in range(3):
+            v, r = S.system(st, scatter=sc)
+            assert torch.equal(v, ref_v) and torch.equal(r, ref_r)
+    finally:
+        del os.environ["FEM_NS_DET"]
     S.close()
 
 
