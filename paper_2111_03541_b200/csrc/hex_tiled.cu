@@ -345,6 +345,7 @@ static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
 }
 
 constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
+constexpr int HEX_MAX_VISITS = 256;  // domain visits of one tile when boundary terms run inside the visits
 constexpr int HEX_SCRATCH = 200;  // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
 // exchanged gradient G_a,i(ξ_q) in the warp scratch: [i][q][a], a swizzled by bit 1 of q; w at 192 + q
 __device__ __forceinline__ constexpr int hx_gx(int i, int q, int a) { return 64 * i + 8 * q + (a ^ (4 * ((q >> 1) & 1))); }
@@ -542,6 +543,115 @@ struct TileOffs {
 // and c+4 (6) for lane l = 4a + c; ∇̂N_c and ∇̂N_(c+4) at point q (6) for l = 4q + c.
 constexpr int LANE_TAB = 18;
 
+// Boundary terms of the elasticity problem inside the owning element's visit ("boundary conditions are
+// just the domain physics one dimension lower"; reading L18), for the forms of P:920-922:
+// ELAST_FIX_ALL / ELAST_FIX_D1 (penalty τ, prescribed dʷ) add -f0 τ Σ_γ w N_a N_b δ_im to the lane's K
+// entries and τ N_a (dʷ_i - d_i) to row (a, i) of the residual; ELAST_LOAD adds N_a σˡ_ij n_j.  Face
+// points: Gauss-Legendre 2x2 on face f (axis f >> 1, side ±1; reading L8, L9); w = |det J J^-T m̂| and
+// n = det J J^-T m̂ / w (Nanson).  fm holds bit 6 k + f for each face f of the element in boundary set k.
+// Lane (a, c) receives K contributions in Kv (columns b = 2c + t) and fres[i] for its row a.
+template <bool HAS_V, bool HAS_R>
+__device__ __forceinline__ void hex_el_facets(const TiledParams& P, uint32_t fm, const double* hdat, int HH,
+                                              const uint16_t* hv, double* sc, double (&Kv)[2][9], double (&fres)[3]) {
+  const int lane = threadIdx.x & 31;
+  const int a = lane >> 2, c = lane & 3;
+  const double r = 0.57735026918962576451;
+  for (int f = 0; f < P.n_fac; f++) {
+    const FormArgs& F = P.fac[f];
+    uint32_t faces = (fm >> (6 * P.fac_set[f])) & 63u;
+    while (faces) {
+      const int face = __ffs(faces) - 1;
+      faces &= faces - 1;
+      const int axis = face >> 1, a1 = (axis + 1) % 3, a2 = (axis + 2) % 3;
+      const double side = (face & 1) ? 1.0 : -1.0;
+      {  // geometry at face point q = lane >> 3 from node an = lane & 7 (reduced over the 8 lanes of q)
+        const int q = lane >> 3, an = lane & 7;
+        double xi[3];
+        xi[axis] = side;
+        xi[a1] = (q & 1) ? r : -r;
+        xi[a2] = (q & 2) ? r : -r;
+        const double sx = hex_sign(an, 0), sy = hex_sign(an, 1), sz = hex_sign(an, 2);
+        const double fx = 0.5 * (1.0 + sx * xi[0]), fy = 0.5 * (1.0 + sy * xi[1]), fz = 0.5 * (1.0 + sz * xi[2]);
+        const double Nn = fx * fy * fz, g[3] = {0.5 * sx * fy * fz, 0.5 * sy * fx * fz, 0.5 * sz * fx * fy};
+        const int h = hv[an];
+        double J[3][3], dq[3];
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+          const double X = hdat[i * HH + h];
+#pragma unroll
+          for (int j = 0; j < 3; j++) J[i][j] = X * g[j];
+          dq[i] = HAS_R ? Nn * hdat[(3 + i) * HH + h] : 0.0;
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+          for (int i = 0; i < 3; i++) {
+#pragma unroll
+            for (int j = 0; j < 3; j++) J[i][j] += __shfl_xor_sync(0xffffffffu, J[i][j], o);
+            if (HAS_R) dq[i] += __shfl_xor_sync(0xffffffffu, dq[i], o);
+          }
+        }
+        // Nanson: n dA = det J J^-T m̂, m̂ = side e_axis, so n_i dA = side (cofactor of J)_(i, axis)
+        double cof[3];
+        cof[0] = J[1][(axis + 1) % 3] * J[2][(axis + 2) % 3] - J[1][(axis + 2) % 3] * J[2][(axis + 1) % 3];
+        cof[1] = J[2][(axis + 1) % 3] * J[0][(axis + 2) % 3] - J[2][(axis + 2) % 3] * J[0][(axis + 1) % 3];
+        cof[2] = J[0][(axis + 1) % 3] * J[1][(axis + 2) % 3] - J[0][(axis + 2) % 3] * J[1][(axis + 1) % 3];
+        const double nn = side * side * (cof[0] * cof[0] + cof[1] * cof[1] + cof[2] * cof[2]);
+        const double dA = sqrt(nn);
+        if (an == 0) {
+          double* o = sc + q * 8;
+          o[0] = dA;  // w: unit Gauss-Legendre weights
+#pragma unroll
+          for (int i = 0; i < 3; i++) { o[1 + i] = side * cof[i] / dA; o[4 + i] = dq[i]; }
+        }
+      }
+      __syncwarp();
+      const double tau = F.p[0];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const double* o = sc + q * 8;
+        double xi[3];
+        xi[axis] = side;
+        xi[a1] = (q & 1) ? r : -r;
+        xi[a2] = (q & 2) ? r : -r;
+        auto Nf = [&](int n) {
+          return 0.125 * (1.0 + hex_sign(n, 0) * xi[0]) * (1.0 + hex_sign(n, 1) * xi[1]) * (1.0 + hex_sign(n, 2) * xi[2]);
+        };
+        const double w = o[0], Na = Nf(a);
+        if (F.form == FEM_WF_ELAST_FIX_ALL || F.form == FEM_WF_ELAST_FIX_D1) {
+          if constexpr (HAS_V) {
+#pragma unroll
+            for (int t = 0; t < 2; t++) {
+              const double kk = -F.f0 * tau * w * Na * Nf(2 * c + t);
+              if (F.form == FEM_WF_ELAST_FIX_ALL) {
+#pragma unroll
+                for (int i = 0; i < 3; i++) Kv[t][i * 3 + i] += kk;
+              } else {
+                Kv[t][0] += kk;
+              }
+            }
+          }
+          if constexpr (HAS_R) {
+            if (F.form == FEM_WF_ELAST_FIX_ALL) {
+#pragma unroll
+              for (int i = 0; i < 3; i++) fres[i] += w * tau * Na * (F.p[1 + i] - o[4 + i]);
+            } else {
+              fres[0] += w * tau * Na * (F.p[1] - o[4]);
+            }
+          }
+        } else if (F.form == FEM_WF_ELAST_LOAD) {
+          if constexpr (HAS_R) {
+#pragma unroll
+            for (int i = 0; i < 3; i++)
+              fres[i] += w * Na * (F.p[3 * i] * o[1] + F.p[3 * i + 1] * o[2] + F.p[3 * i + 2] * o[3]);
+          }
+        }
+      }
+      __syncwarp();  // the face-point scratch is rewritten by the next face
+    }
+  }
+}
+
 // Call kinds, fixed per launch so each visit body is compiled lean: matrix only, residual only, system with
 // the residual fused into the scatter (f0 = 1), system with the stress-GEMM residual (f0 != 1).
 enum { HX_MAT = 0, HX_RES = 1, HX_SYS_FUSED = 2, HX_SYS = 3 };
@@ -549,7 +659,7 @@ enum { HX_MAT = 0, HX_RES = 1, HX_SYS_FUSED = 2, HX_SYS = 3 };
 template <bool DET, int MODE, bool ORDERED = DET>
 __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOffs& to, const HexCoef& H,
                                               const double* __restrict__ lt, double* sc, int v,
-                                              unsigned char* sm) {
+                                              unsigned char* sm, const uint32_t* vfm) {
   const int lane = threadIdx.x & 31;
   const int16_t* own = reinterpret_cast<const int16_t*>(sm + to.vown) + v * 8;
   const uint16_t* hv = reinterpret_cast<const uint16_t*>(sm + to.vhal) + v * 8;
@@ -737,6 +847,14 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       for (int i = 0; i < 3; i++) res[i] = sum4(res[i]);
     }
   }
+  double fres[3] = {0.0, 0.0, 0.0};  // boundary-term residual of row a (every lane of the row)
+  if (vfm) {
+    const uint32_t fm = vfm[v];
+    if (fm) {
+      __syncwarp();  // every lane is done with the per-point records in the scratch
+      hex_el_facets<has_values, has_rhs>(P, fm, hdat, HH, hv, sc, Kv, fres);
+    }
+  }
   int* turn = reinterpret_cast<int*>(sm + to.turn);
   int my_turn = 0;
   if constexpr (ORDERED) {  // wait for this visit's turn on the owned row it writes (record order)
@@ -751,11 +869,11 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     if (has_rhs && !fuse && c < 2 && li >= 0) {
       double* racc = reinterpret_cast<double*>(sm + to.racc) + li + 2 * c * to.T;
       if constexpr (DET) {
-        racc[0] -= res[0];
-        if (c == 0) racc[to.T] -= res[1];
+        racc[0] += (c == 0 ? fres[0] : fres[2]) - res[0];
+        if (c == 0) racc[to.T] += fres[1] - res[1];
       } else {
-        atomicAdd(racc, -res[0]);
-        if (c == 0) atomicAdd(racc + to.T, -res[1]);
+        atomicAdd(racc, (c == 0 ? fres[0] : fres[2]) - res[0]);
+        if (c == 0) atomicAdd(racc + to.T, fres[1] - res[1]);
       }
     }
   };
@@ -787,8 +905,8 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
           double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
 #pragma unroll
           for (int i = 0; i < 3; i++) {
-            if constexpr (DET) racc[i * to.T] += res[i];
-            else atomicAdd(racc + i * to.T, res[i]);
+            if constexpr (DET) racc[i * to.T] += res[i] + fres[i];
+            else atomicAdd(racc + i * to.T, res[i] + fres[i]);
           }
         }
       }
@@ -809,8 +927,9 @@ constexpr int HEX_WARPS = HEX_THREADS / 32;
 
 template <bool DET, int MODE>
 __device__ __forceinline__ void hex_visits(const TiledParams& P, const TileOffs& to, const HexCoef& Hc,
-                                           const double* lanetab, double* wsc, unsigned char* smem, int nv, int warp) {
-  for (int v = warp; v < nv; v += HEX_WARPS) hex_visit_el2<DET, MODE>(P, to, Hc, lanetab, wsc, v, smem);  // static split
+                                           const double* lanetab, double* wsc, unsigned char* smem, int nv, int warp,
+                                           const uint32_t* vfm) {
+  for (int v = warp; v < nv; v += HEX_WARPS) hex_visit_el2<DET, MODE>(P, to, Hc, lanetab, wsc, v, smem, vfm);  // static split
 }
 
 template <int KH, bool DET>
@@ -821,6 +940,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
   int* ctr = reinterpret_cast<int*>(smem + 64);
   __shared__ TileOffs to;
   __shared__ double lanetab[32 * LANE_TAB];
+  __shared__ uint32_t vfmask[HEX_MAX_VISITS];  // in-visit boundary terms: bit 6 k + face per domain visit
 #define RBUF(i) (smem + 128 + (size_t)(i) * P.rec_cap)
 #define HBUF(i) (reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap) + (size_t)(i) * P.hcap)
   double* acc = HBUF(2);
@@ -923,18 +1043,30 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
       reinterpret_cast<double2*>(acc)[i] = make_double2(0.0, 0.0);
     if constexpr (DET)
       for (int i = tid; i < T; i += blockDim.x) turn[i] = 0;
+    const bool finl = P.fac_inline && fmask;
+    if (finl)
+      for (int i = tid; i < nv; i += blockDim.x) vfmask[i] = 0u;
     cp_async_wait_all();
     __syncthreads();
+    if (finl) {  // facet visit i of set k is face ffac[i] of domain visit fdv[i] (record layout)
+      const int32_t* fcnt = reinterpret_cast<const int32_t*>(rec + L.o_fcnt);
+      const int16_t* fdv = reinterpret_cast<const int16_t*>(rec + L.o_fdv);
+      const int8_t* ffac = reinterpret_cast<const int8_t*>(rec + L.o_ffac);
+      for (int k = 0; k < hdr[6]; k++)
+        for (int i = fcnt[k] + tid; i < fcnt[k + 1]; i += blockDim.x) atomicOr(&vfmask[fdv[i]], 1u << (6 * k + ffac[i]));
+      __syncthreads();
+    }
+    const uint32_t* vf = finl ? vfmask : nullptr;
     const int32_t* run = reinterpret_cast<const int32_t*>(rec + L.o_run);
     double* wsc = reinterpret_cast<double*>(F.qp) + (size_t)HEX_SCRATCH * warp;
     if constexpr (KH == 3) {
       // DET: visit v takes its turn on each accumulator row it writes (vseq), so every entry sums its
       // contributions in record order with plain adds, without block-wide barriers between colours
       switch (hmode) {
-        case HX_MAT: hex_visits<DET, HX_MAT>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
-        case HX_RES: hex_visits<DET, HX_RES>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
-        case HX_SYS_FUSED: hex_visits<DET, HX_SYS_FUSED>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
-        default: hex_visits<DET, HX_SYS>(P, to, Hc, lanetab, wsc, smem, nv, warp); break;
+        case HX_MAT: hex_visits<DET, HX_MAT>(P, to, Hc, lanetab, wsc, smem, nv, warp, vf); break;
+        case HX_RES: hex_visits<DET, HX_RES>(P, to, Hc, lanetab, wsc, smem, nv, warp, vf); break;
+        case HX_SYS_FUSED: hex_visits<DET, HX_SYS_FUSED>(P, to, Hc, lanetab, wsc, smem, nv, warp, vf); break;
+        default: hex_visits<DET, HX_SYS>(P, to, Hc, lanetab, wsc, smem, nv, warp, vf); break;
       }
     } else if constexpr (DET) {
       for (int r = 0; r < nr; r++) {  // colour runs: conflict-free, plain shared-memory adds
@@ -962,7 +1094,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
     F.vloc = V.vloc;
     F.hdat = const_cast<double*>(V.hdat);
     F.H = H;
-    if (fmask)  // DET: node-disjoint facet segments, one barrier each
+    if (fmask && !P.fac_inline)  // DET: node-disjoint facet segments, one barrier each
       rec_facets<ET_HEX, 1, KH, 2, FACET_WARPS, DET>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
     tile_epilogue<KH>(P, F);
     __syncthreads();
@@ -988,6 +1120,13 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
   P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
   P.spin_ns = getenv("FEM_SPIN_NS") ? atoi(getenv("FEM_SPIN_NS")) : 0;
+  // elasticity boundary terms (fix / load) inside the owning element's visit: no facet phase, no barriers
+  P.fac_inline = KH == 3 && T.dom.max_per_tile <= HEX_MAX_VISITS && !getenv("FEM_HEX_FACET_PHASE");
+  for (int f = 0; f < P.n_fac; f++) {
+    const int fo = P.fac[f].form;
+    if ((fo != FEM_WF_ELAST_FIX_ALL && fo != FEM_WF_ELAST_FIX_D1 && fo != FEM_WF_ELAST_LOAD) || P.fac_set[f] > 4)
+      P.fac_inline = 0;
+  }
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * FACET_WARPS, (size_t)8 * HEX_SCRATCH * HEX_WARPS) + (size_t)fv * (4 + 8 * 4 + 8 * 2 + 1) + 16;
   const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + fac_bytes;
   cudaFuncAttributes fa;

@@ -49,6 +49,7 @@ struct TiledParams {
   int turn_cap;  // ints of the per-row turn counters (ordered deterministic kernels), multiple of 4
   int spin_ns;   // back-off of a visit waiting for its turn (FEM_SPIN_NS, default 0 = spin)
   int fvmax;     // capacity of the facet visit arrays
+  int fac_inline;  // hex elasticity: boundary terms integrated inside the owning element's visit
 };
 
 // Lean point record for elasticity-only domain visits: w, ∇N_a, and w·σ.

@@ -146,6 +146,45 @@ def test_genalpha_elasticity_f0(name):
     S.close()
 
 
+@pytest.mark.parametrize("variant", ["structured", "perturbed"])
+def test_hex_elasticity_boundary_terms_every_face(variant):
+    """Q1 hex elasticity with FIX_D1 / FIX_ALL (non-zero dʷ) / LOAD (full σˡ) on faces of every axis and
+    both sides, an element with two boundary faces in one set, and two terms on one set:
+    the tiled kernel integrates them inside the element visits; the generic facet phase
+    (FEM_HEX_FACET_PHASE) and the atomic / coloured paths must agree with the oracle."""
+    _need_gpu()
+    from fem_inputs.configs import Term
+    from fem_inputs.meshgen import facets_on_plane
+    m, p = make_config("c5", variant, SMALL["c5"])
+    xm, xp, ym, zp = (facets_on_plane(m, 0, 0.0), facets_on_plane(m, 0, 1.0), facets_on_plane(m, 1, 0.0),
+                      facets_on_plane(m, 2, 1.0))
+    both = (np.concatenate([xp[0], zp[0]]).astype(np.int32), np.concatenate([xp[1], zp[1]]).astype(np.int8))
+    m.bsets = [xm, ym, both]
+    m.bset_names = ["x0", "y0", "x1_z1"]
+    sl = (1e-3, -2e-4, 3e-4, -2e-4, 5e-4, 1e-4, 3e-4, 1e-4, -7e-4)
+    p.terms = [p.terms[0],
+               Term("ELAST_FIX_D1", 0, dict(tau=2e3, dw=(1e-3,))),
+               Term("ELAST_FIX_ALL", 1, dict(tau=1e3, dw=(1e-3, -2e-3, 5e-4))),
+               Term("ELAST_LOAD", 2, dict(sigma_l=sl)),
+               Term("ELAST_FIX_ALL", 2, dict(tau=5e2, dw=(0.0, 1e-3, 0.0)))]
+    st = make_state("c5", m, p)
+    ora = oracle.assemble(m, p, st)
+    assert ora["status"] == 0
+    for phase in ("", "1"):
+        if phase:
+            os.environ["FEM_HEX_FACET_PHASE"] = phase
+        try:
+            S = _gpu_system(m, p)
+            sd = _to_dev(st)
+            for sc in SCATTERS:
+                for v, r in [S.system(sd, scatter=sc), (S.matrix(sd, scatter=sc).clone(), S.residual(sd, scatter=sc).clone())]:
+                    assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL, (sc, phase)
+                    assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL, (sc, phase)
+            S.close()
+        finally:
+            os.environ.pop("FEM_HEX_FACET_PHASE", None)
+
+
 def test_inverted_element_reported_and_edge_cases():
     _need_gpu()
     from helpers import REF_TET, one_element, problem
