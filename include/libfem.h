@@ -178,6 +178,34 @@ int fem_mesh_info(fem_mesh_t mesh, int* n_loc, int* kappa_hat, int* n_colours, i
  * [7] total packed record bytes. */
 int fem_pattern_info(fem_pattern_t pat, int64_t* out8);
 
+/* ---- NEXT-1: the linear solve of the Newton sub-step, D-4 ----------------
+ * The linearisation K Δφ = -d of d(φ) = 0 is solved on the CSR of fem_pattern_build.
+ *
+ * fem_spmv — y = alpha·K·x + beta·y for the CSR K (rowptr int64 [n_rows+1], colidx int32 [nnz], values
+ *   fp64 [nnz], all DEVICE; x, y DEVICE fp64, x indexed by column).  Stream-ordered, no sync.
+ *   Single-GPU pattern (columns index the same vector as rows).  FEM_E_INVALID_ARG on NULL / n_rows < 0.
+ *
+ * fem_cg_work_doubles — size of the caller-owned DEVICE work buffer of fem_cg_solve, in doubles.
+ *
+ * fem_cg_solve — Jacobi-preconditioned conjugate gradients for K x = b, run on (s K) x = s b with
+ *   s = spd_sign = ±1 chosen by the caller so that s K is symmetric positive definite (thermal and
+ *   elasticity with penalty boundary terms: s = -1, reading L17).  x (DEVICE) holds the initial guess on
+ *   entry and the solution on exit; b DEVICE.  Stops when ||r||_2 <= rtol ||r_0||_2 or after max_iter
+ *   iterations; the convergence test is read back every check_every iterations (<= 0: 16), so the call
+ *   synchronizes `stream` (the only host syncs).  iters_out / relres_out (host, may be NULL) receive the
+ *   iteration count and ||r||/||r_0||.  Every reduction sums in fixed order: bit-identical run to run.
+ *   Errors: FEM_E_INVALID_ARG for bad arguments or a non-positive diagonal of s K (not SPD). */
+/* fem_pattern_csr — the pattern's own DEVICE CSR arrays (library-owned, valid until fem_pattern_destroy,
+ *   read-only): rowptr int64 [n_rows+1], colidx int32 [nnz] (global column ids; *col_offset = own_lo, 0
+ *   on a single GPU).  No copy, no sync. */
+int fem_pattern_csr(fem_pattern_t pat, const int64_t** rowptr, const int32_t** colidx, int64_t* col_offset);
+int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+             const double* x, double* y, double alpha, double beta, void* stream);
+int64_t fem_cg_work_doubles(int64_t n_rows);
+int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+                 const double* b, double* x, double spd_sign, int max_iter, double rtol, int check_every,
+                 double* work, int* iters_out, double* relres_out, void* stream);
+
 void fem_pattern_destroy(fem_pattern_t pat);
 void fem_mesh_destroy(fem_mesh_t mesh);
 const char* fem_last_error(void);

@@ -281,6 +281,14 @@ int fem_pattern_export(fem_pattern_t p, int64_t* rowptr, int32_t* colidx, int32_
   return 0;
 }
 
+int fem_pattern_csr(fem_pattern_t p, const int64_t** rowptr, const int32_t** colidx, int64_t* col_offset) {
+  if (!p || !rowptr || !colidx) { set_error("fem_pattern_csr: NULL argument"); return FEM_E_INVALID_ARG; }
+  *rowptr = p->rowptr;
+  *colidx = p->colidx;
+  if (col_offset) *col_offset = p->mesh->own_lo;
+  return 0;
+}
+
 static int check_problem(const fem_mesh_s* m, const fem_problem* prob) {
   if (!prob) { set_error("NULL problem"); return FEM_E_INVALID_ARG; }
   if (prob->etype != m->etype || prob->order != m->order || prob->physics != m->physics) {

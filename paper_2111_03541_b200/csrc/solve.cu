@@ -1,0 +1,268 @@
+// solve.cu — NEXT-1: the linear solve of the Newton sub-step on the GPU.
+//
+// PAPER.md D-4 solves the assembled system for the increment, K Δφ = -d (the
+// linearisation of d(φ) = 0), then updates the control-point values.  For the thermal and elasticity
+// forms K is symmetric and, with the paper's sign convention (reading L17), negative definite once the
+// penalty terms fix the rigid modes, so s·K with s = -1 is symmetric positive definite and the solve is
+// Jacobi-preconditioned conjugate gradients on (s K) x = s b.  The kernels are HBM-bound sparse/vector
+// passes over the CSR of fem_pattern_build: the SpMV moves 12 B per nnz (fp64 value + int32 column) and
+// the vector updates a few doubles per row.  Dot products reduce per block into a partials array whose
+// last-arriving block sums it in fixed order, so every iteration is bit-identical run to run.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "fem_internal.cuh"
+
+namespace fem {
+
+constexpr int SV_THREADS = 256;
+constexpr int SV_MAX_BLOCKS = 148 * 8;  // vector kernels: persistent grid, a multiple of the SM count
+
+// device scalars of one CG solve (in the caller's work buffer after the 5 vectors)
+struct CgScal {
+  double rz, rz_new, pq, rr, rr0, alpha, beta;
+  unsigned int count0, count1;  // last-block tickets of the two reducing kernels
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-sum of v, then the last block to arrive sums the per-block partials in block order.
+// Returns true in thread 0 of that last block, with *out written.
+__device__ __forceinline__ bool block_reduce_last(double v, double* partials, unsigned int* ticket, double* out) {
+  __shared__ double ws[SV_THREADS / 32];
+  __shared__ bool last;
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < SV_THREADS / 32; i++) b += ws[i];
+    partials[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned i = 0; i < gridDim.x; i++) t += reinterpret_cast<volatile double*>(partials)[i];
+    *out = t;
+    *ticket = 0u;
+  }
+  return threadIdx.x == 0;
+}
+
+// y = alpha K x + beta y: G lanes per row (G = 8: 81-entry Q1 elasticity rows take ~10 loads per lane),
+// lanes read consecutive entries of the row, sub-warp shuffle reduction.  The row loop is uniform per
+// warp (32 / G rows per warp and step), so the shuffles never see an exited lane.
+template <int G>
+__device__ __forceinline__ double row_dot(int64_t r, int64_t n, int sub, const int64_t* __restrict__ rowptr,
+                                          const int32_t* __restrict__ colidx, const double* __restrict__ val,
+                                          const double* __restrict__ x) {
+  double acc = 0.0;
+  if (r < n)
+    for (int64_t k = rowptr[r] + sub; k < rowptr[r + 1]; k += G) acc = fma(__ldcs(val + k), __ldg(x + __ldcs(colidx + k)), acc);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+  return acc;
+}
+
+template <int G>
+__global__ void __launch_bounds__(SV_THREADS) k_spmv(int64_t n, const int64_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ colidx,
+                                                     const double* __restrict__ val, const double* __restrict__ x,
+                                                     double* __restrict__ y, double alpha, double beta) {
+  constexpr int RPW = 32 / G;  // rows per warp and step
+  const int lane = threadIdx.x & 31, sub = lane % G;
+  const int64_t nwarps = (int64_t)gridDim.x * (SV_THREADS / 32);
+  for (int64_t w = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) / 32; w * RPW < n; w += nwarps) {
+    const int64_t r = w * RPW + lane / G;
+    const double acc = row_dot<G>(r, n, sub, rowptr, colidx, val, x);
+    if (sub == 0 && r < n) y[r] = alpha * acc + (beta == 0.0 ? 0.0 : beta * y[r]);
+  }
+}
+
+// q = s K p and pq = p·q
+template <int G>
+__global__ void __launch_bounds__(SV_THREADS) k_cg_spmv(int64_t n, const int64_t* __restrict__ rowptr,
+                                                        const int32_t* __restrict__ colidx,
+                                                        const double* __restrict__ val, double s,
+                                                        const double* __restrict__ p, double* __restrict__ q,
+                                                        double* partials, CgScal* sc) {
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31, sub = lane % G;
+  const int64_t nwarps = (int64_t)gridDim.x * (SV_THREADS / 32);
+  double dot = 0.0;
+  for (int64_t w = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) / 32; w * RPW < n; w += nwarps) {
+    const int64_t r = w * RPW + lane / G;
+    const double acc = row_dot<G>(r, n, sub, rowptr, colidx, val, p);
+    if (sub == 0 && r < n) {
+      const double qr = s * acc;
+      q[r] = qr;
+      dot = fma(p[r], qr, dot);
+    }
+  }
+  double pq;
+  if (block_reduce_last(dot, partials, &sc->count0, &pq)) {
+    sc->pq = pq;
+    sc->rz = sc->rz_new;  // every block of the previous k_cg_dir has used the old rz (stream order)
+    sc->alpha = sc->rz / pq;
+  }
+}
+
+// x += α p, r -= α q, z = D^-1 r; rz_new = r·z and rr = r·r (two reductions through one partials row each)
+__global__ void __launch_bounds__(SV_THREADS) k_cg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                          const double* __restrict__ p, const double* __restrict__ q,
+                                                          const double* __restrict__ dinv, double* __restrict__ z,
+                                                          double* partials, CgScal* sc) {
+  const double alpha = sc->alpha;
+  double rz = 0.0, rr = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    const double zi = dinv[i] * ri;
+    z[i] = zi;
+    rz = fma(ri, zi, rz);
+    rr = fma(ri, ri, rr);
+  }
+  // pack the two sums: reduce rz into partials[0..grid), rr into partials[grid..2 grid)
+  double out;
+  if (block_reduce_last(rz, partials, &sc->count0, &out)) {
+    sc->rz_new = out;
+  }
+  __syncthreads();
+  if (block_reduce_last(rr, partials + gridDim.x, &sc->count1, &out)) {
+    sc->rr = out;
+  }
+}
+
+// p = z + β p with β = rz_new / rz (rz ← rz_new happens in the next k_cg_spmv)
+__global__ void __launch_bounds__(SV_THREADS) k_cg_dir(int64_t n, const double* __restrict__ z, double* __restrict__ p,
+                                                       CgScal* sc, int first) {
+  const double beta = first ? 0.0 : sc->rz_new / sc->rz;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS)
+    p[i] = first ? z[i] : fma(beta, p[i], z[i]);
+}
+
+// r = b - s K x (x the initial guess), z = D^-1 r, dinv from the diagonal of s K
+__global__ void __launch_bounds__(SV_THREADS) k_cg_init(int64_t n, const int64_t* __restrict__ rowptr,
+                                                        const int32_t* __restrict__ colidx,
+                                                        const double* __restrict__ val, double s,
+                                                        const double* __restrict__ b, const double* __restrict__ x,
+                                                        double* __restrict__ r, double* __restrict__ z,
+                                                        double* __restrict__ dinv, double* partials, CgScal* sc,
+                                                        int* bad_diag) {
+  double rz = 0.0, rr = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS) {
+    double ax = 0.0, dg = 0.0;
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; k++) {
+      const int32_t c = colidx[k];
+      ax = fma(val[k], x[c], ax);
+      if (c == i) dg = val[k];
+    }
+    dg *= s;
+    if (!(dg > 0.0)) atomicExch(bad_diag, 1);
+    const double di = 1.0 / dg;
+    dinv[i] = di;
+    const double ri = s * b[i] - s * ax;
+    r[i] = ri;
+    z[i] = di * ri;
+    rz = fma(ri, di * ri, rz);
+    rr = fma(ri, ri, rr);
+  }
+  double out;
+  if (block_reduce_last(rz, partials, &sc->count0, &out)) {
+    sc->rz_new = out;
+  }
+  __syncthreads();
+  if (block_reduce_last(rr, partials + gridDim.x, &sc->count1, &out)) {
+    sc->rr = out;
+    sc->rr0 = out;
+  }
+}
+
+static int grid_for(int64_t n, int per_thread_rows) {
+  const int64_t need = (n * per_thread_rows + SV_THREADS - 1) / SV_THREADS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, SV_MAX_BLOCKS));
+}
+
+}  // namespace fem
+
+using namespace fem;
+
+extern "C" int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+                        const double* x, double* y, double alpha, double beta, void* stream) {
+  if (n_rows < 0 || (n_rows > 0 && (!rowptr || !colidx || !values || !x || !y))) {
+    set_error("fem_spmv: invalid argument");
+    return FEM_E_INVALID_ARG;
+  }
+  if (n_rows == 0) return 0;
+  k_spmv<8><<<grid_for(n_rows, 8), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int64_t fem_cg_work_doubles(int64_t n_rows) {
+  return 5 * n_rows + 2 * SV_MAX_BLOCKS + (int64_t)(sizeof(CgScal) + 7) / 8 + 8;
+}
+
+extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+                            const double* b, double* x, double spd_sign, int max_iter, double rtol, int check_every,
+                            double* work, int* iters_out, double* relres_out, void* stream) {
+  if (n_rows <= 0 || !rowptr || !colidx || !values || !b || !x || !work || max_iter < 0 || !(rtol >= 0.0) ||
+      (spd_sign != 1.0 && spd_sign != -1.0)) {
+    set_error("fem_cg_solve: invalid argument (n_rows > 0, non-NULL pointers, spd_sign = ±1, rtol >= 0)");
+    return FEM_E_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = n_rows;
+  double* r = work;
+  double* z = r + n;
+  double* p = z + n;
+  double* q = p + n;
+  double* dinv = q + n;
+  double* partials = dinv + n;
+  CgScal* sc = reinterpret_cast<CgScal*>(partials + 2 * SV_MAX_BLOCKS);
+  int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(CgScal));
+  FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(CgScal) + 8, s));
+  const int gv = grid_for(n, 1), gm = grid_for(n, 8);
+  k_cg_init<<<gv, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, b, x, r, z, dinv, partials, sc, bad);
+  k_cg_dir<<<gv, SV_THREADS, 0, s>>>(n, z, p, sc, 1);
+  FEM_CUDA_TRY(cudaGetLastError());
+  CgScal h{};
+  int hbad = 0;
+  FEM_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof(CgScal), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hbad) {
+    set_error("fem_cg_solve: a diagonal entry of spd_sign*K is not positive (matrix not SPD with this sign)");
+    return FEM_E_INVALID_ARG;
+  }
+  const double rr0 = h.rr0;
+  int it = 0;
+  double rel = rr0 > 0.0 ? 1.0 : 0.0;
+  const int chk = check_every > 0 ? check_every : 16;
+  while (rr0 > 0.0 && it < max_iter && rel > rtol) {
+    const int todo = std::min(chk, max_iter - it);
+    for (int k = 0; k < todo; k++) {
+      k_cg_spmv<8><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
+      k_cg_update<<<gv, SV_THREADS, 0, s>>>(n, x, r, p, q, dinv, z, partials, sc);
+      k_cg_dir<<<gv, SV_THREADS, 0, s>>>(n, z, p, sc, 0);
+    }
+    FEM_CUDA_TRY(cudaGetLastError());
+    it += todo;
+    FEM_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof(CgScal), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA_TRY(cudaStreamSynchronize(s));
+    rel = sqrt(h.rr / rr0);
+  }
+  if (iters_out) *iters_out = it;
+  if (relres_out) *relres_out = rel;
+  return 0;
+}

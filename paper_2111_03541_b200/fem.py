@@ -126,6 +126,12 @@ def lib():
         L.fem_pattern_destroy.restype = None
         L.fem_mesh_destroy.argtypes = [V]
         L.fem_mesh_destroy.restype = None
+        L.fem_pattern_csr.argtypes = [V, C.POINTER(V), C.POINTER(V), C.POINTER(I64)]
+        L.fem_spmv.argtypes = [I64, V, V, V, V, V, C.c_double, C.c_double, V]
+        L.fem_cg_work_doubles.argtypes = [I64]
+        L.fem_cg_work_doubles.restype = I64
+        L.fem_cg_solve.argtypes = [I64, V, V, V, V, V, C.c_double, I, C.c_double, I, V, C.POINTER(I),
+                                   C.POINTER(C.c_double), V]
         L.fem_last_error.restype = C.c_char_p
         L.fem_version.restype = I
         _lib = L
@@ -135,7 +141,8 @@ def lib():
 EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pattern_export", "fem_pattern_info",
             "fem_assemble_matrix", "fem_assemble_residual", "fem_assemble_system", "fem_residual_norms",
             "fem_linearize_host", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
-            "fem_mesh_destroy", "fem_last_error", "fem_version"]
+            "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
+            "fem_cg_work_doubles", "fem_cg_solve"]
 
 
 def _check(rc):
@@ -240,6 +247,32 @@ def fem_linearize_host(mesh_h, pat_h, problem, state_host, values, rhs, norms_ho
     P = P if P is not None else make_problem(problem)
     _check(lib().fem_linearize_host(mesh_h, pat_h, C.byref(P), _ptr(state_host), _ptr(values), _ptr(rhs),
                                     _ptr(norms_host), SCATTER[scatter], _stream(stream)))
+
+
+def fem_pattern_csr(pat_h):
+    """Library-owned device CSR of the pattern: (rowptr ptr, colidx ptr, column offset)."""
+    rp, ci, off = C.c_void_p(), C.c_void_p(), C.c_int64()
+    _check(lib().fem_pattern_csr(pat_h, C.byref(rp), C.byref(ci), C.byref(off)))
+    return rp.value, ci.value, off.value
+
+
+def fem_spmv(n_rows, rowptr, colidx, values, x, y, alpha=1.0, beta=0.0, stream=None):
+    _check(lib().fem_spmv(int(n_rows), _ptr(rowptr), _ptr(colidx), _ptr(values), _ptr(x), _ptr(y), float(alpha),
+                          float(beta), _stream(stream)))
+
+
+def fem_cg_work_doubles(n_rows):
+    return int(lib().fem_cg_work_doubles(int(n_rows)))
+
+
+def fem_cg_solve(n_rows, rowptr, colidx, values, b, x, work, spd_sign=-1.0, max_iter=10000, rtol=1e-12,
+                 check_every=16, stream=None):
+    """Jacobi-PCG for K x = b on (spd_sign K) x = spd_sign b; returns (iterations, ||r||/||r0||)."""
+    it, rel = C.c_int(0), C.c_double(0.0)
+    _check(lib().fem_cg_solve(int(n_rows), _ptr(rowptr), _ptr(colidx), _ptr(values), _ptr(b), _ptr(x),
+                              float(spd_sign), int(max_iter), float(rtol), int(check_every), _ptr(work),
+                              C.byref(it), C.byref(rel), _stream(stream)))
+    return it.value, rel.value
 
 
 def fem_get_status(mesh_h, stream=None):

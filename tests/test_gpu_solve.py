@@ -1,0 +1,113 @@
+"""NEXT-1: the Newton sub-step's linear solve on the GPU, through the C ABI.
+
+D-4 solves K Δφ = -d.  The GPU path is fem_spmv / fem_cg_solve (Jacobi-PCG on
+s K with s = -1: the elasticity K is symmetric negative definite in the paper's sign convention,
+reading L17).  Pins:
+  * fem_spmv against scipy's CSR product of the ORACLE's K (same pattern, bit-exact, see the parity
+    tests), within a sum-of-|terms| bound;
+  * the CG solution against scipy's direct solve of the oracle's system, within κ(A)·rtol;
+  * linearity: the elasticity form is linear in d, so ONE Newton step from any state zeroes the
+    residual (the D-2 convergence test);
+  * mathematics: a P2-tet cantilever (the c3 beam with ν = 0, as the paper's beam P:944) deflects by
+    Timoshenko's P L³/(3 E I) + P L/(κ G A) (I = h⁴/12, reading L24; κ = 5/6) to 0.5 %.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from fem_inputs import make_config, make_state  # noqa: E402
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _csr(ora):
+    import scipy.sparse as sp
+    n = len(ora["rowptr"]) - 1
+    return sp.csr_matrix((ora["values"], ora["colidx"], ora["rowptr"]), shape=(n, n))
+
+
+@pytest.mark.parametrize("name,dims", [("c1", (8,)), ("c3", (7, 3, 2)), ("c4", (9, 4, 3)), ("c5", (7, 5, 6))])
+def test_spmv_matches_scipy_on_oracle_matrix(name, dims):
+    _need_gpu()
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config(name, "perturbed", dims)
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    S = FemSystem(m, p)
+    S.alloc(True, False)
+    S.values.copy_(torch.from_numpy(ora["values"]))
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, S.n_rows)
+    y0 = rng.uniform(-1, 1, S.n_rows)
+    y = S.spmv(torch.from_numpy(x).cuda(), torch.from_numpy(y0.copy()).cuda(), alpha=0.5, beta=-2.0).cpu().numpy()
+    K = _csr(ora)
+    ref = 0.5 * (K @ x) - 2.0 * y0
+    scale = 0.5 * (abs(K) @ np.abs(x)) + 2.0 * np.abs(y0)
+    assert np.max(np.abs(y - ref) / scale) <= 1e-14
+    S.close()
+
+
+@pytest.mark.parametrize("name,dims", [("c5", (7, 5, 6)), ("c3", (7, 3, 2))])
+def test_cg_matches_direct_solve_and_is_bit_reproducible(name, dims):
+    _need_gpu()
+    import scipy.sparse.linalg as spla
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config(name, "perturbed", dims)
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    K = _csr(ora)
+    x_ref = spla.spsolve(K.tocsc(), -ora["rhs"])
+    S = FemSystem(m, p)
+    sd = torch.from_numpy(st).cuda()
+    Kg, dg = S.system(sd, scatter="tiled")
+    rtol = 1e-13
+    x, it, rel = S.solve(-dg, rtol=rtol, max_iter=50000)
+    assert rel <= rtol and it > 0
+    x = x.cpu().numpy()
+    # forward error <= κ(A) · relative residual (A = -K SPD; dense κ on these small systems)
+    kappa = np.linalg.cond(-K.toarray())
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 10 * kappa * rtol
+    # true residual of the original system (x0 = 0: r0 = b; the recurrence drifts from b - A x by rounding)
+    assert np.linalg.norm(K @ x + ora["rhs"]) / np.linalg.norm(ora["rhs"]) <= 1e-11
+    x2, it2, rel2 = S.solve(-dg, rtol=rtol, max_iter=50000)
+    assert it2 == it and rel2 == rel and np.array_equal(x2.cpu().numpy(), x)
+    S.close()
+
+
+def test_one_newton_step_solves_linear_elasticity():
+    """d(φ) is affine in φ for the elasticity forms, so φ1 = φ0 + Δφ with K Δφ = -d(φ0) zeroes it."""
+    _need_gpu()
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config("c5", "perturbed", (7, 5, 6))
+    st = torch.from_numpy(make_state("c5", m, p)).cuda()
+    S = FemSystem(m, p)
+    _, d0 = S.system(st, scatter="tiled")
+    n0 = float(torch.linalg.norm(d0))
+    st1, it, rel = S.newton_step(st, scatter="tiled", rtol=1e-13)
+    _, d1 = S.system(st1, scatter="tiled")
+    assert float(torch.linalg.norm(d1)) <= 1e-9 * n0
+    S.close()
+
+
+def test_cantilever_tip_deflection_matches_beam_theory():
+    """c3 beam [0,10]x[0,1]^2, P2 tets, ν = 0, fixed at x = 0, end load P = 1e-3."""
+    _need_gpu()
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config("c3", "structured", (40, 4, 4))
+    p.terms[0].params = dict(E=1.0, nu=0.0)
+    S = FemSystem(m, p)
+    st = torch.zeros((1, 3, m.n_nodes), dtype=torch.float64, device="cuda")
+    st1, it, rel = S.newton_step(st, scatter="tiled", rtol=1e-12, max_iter=200000)
+    assert rel <= 1e-12
+    uy = st1[0, 1].cpu().numpy()
+    tip = np.isclose(m.coords[0], 10.0)
+    P, L, E, G, A, I, kappa = 1e-3, 10.0, 1.0, 0.5, 1.0, 1.0 / 12.0, 5.0 / 6.0
+    timoshenko = P * L ** 3 / (3 * E * I) + P * L / (kappa * G * A)
+    assert abs(-uy[tip].mean() / timoshenko - 1.0) <= 5e-3
+    S.close()

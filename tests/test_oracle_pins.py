@@ -483,3 +483,19 @@ def test_ns_tau_reading_L11():
     assert tm == pytest.approx(4.802068e-6, rel=1e-6)
     assert tc == pytest.approx(1.246622, rel=1e-6)
     assert tb == pytest.approx(18.0488, rel=1e-5)
+
+
+def test_cantilever_deflection_timoshenko():
+    """NEXT-1 pin of the oracle: the c3 beam (P2 tets, ν = 0 as the paper's beam P:944) under the end load
+    P = 1e-3 deflects by P L³/(3 E I) + P L/(κ G A), I = h⁴/12 (reading L24), κ = 5/6."""
+    import scipy.sparse as sp
+    m, p = make_config("c3", "structured", (20, 2, 2))
+    p.terms[0].params = dict(E=1.0, nu=0.0)
+    out = oracle.assemble(m, p, np.zeros((1, 3, m.n_nodes)))
+    n = len(out["rowptr"]) - 1
+    K = sp.csr_matrix((out["values"], out["colidx"], out["rowptr"]), shape=(n, n))
+    x = spla.spsolve(K.tocsc(), -out["rhs"])
+    uy = x[m.n_nodes:2 * m.n_nodes]
+    tip = np.isclose(m.coords[0], 10.0)
+    P, L, E, G, A, I, kappa = 1e-3, 10.0, 1.0, 0.5, 1.0, 1.0 / 12.0, 5.0 / 6.0
+    assert abs(-uy[tip].mean() / (P * L ** 3 / (3 * E * I) + P * L / (kappa * G * A)) - 1.0) <= 5e-3
