@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "fem_internal.cuh"
 
@@ -58,16 +59,28 @@ __device__ __forceinline__ bool block_reduce_last(double v, double* partials, un
   return threadIdx.x == 0;
 }
 
-// y = alpha K x + beta y: G lanes per row (G = 8: 81-entry Q1 elasticity rows take ~10 loads per lane),
-// lanes read consecutive entries of the row, sub-warp shuffle reduction.  The row loop is uniform per
+// y = alpha K x + beta y: G lanes per row (default G = 32: an 81-entry Q1 elasticity row is three
+// independent loads per lane), lanes read consecutive entries of the row, (sub-)warp shuffle reduction.  The row loop is uniform per
 // warp (32 / G rows per warp and step), so the shuffles never see an exited lane.
 template <int G>
 __device__ __forceinline__ double row_dot(int64_t r, int64_t n, int sub, const int64_t* __restrict__ rowptr,
                                           const int32_t* __restrict__ colidx, const double* __restrict__ val,
                                           const double* __restrict__ x) {
   double acc = 0.0;
-  if (r < n)
-    for (int64_t k = rowptr[r] + sub; k < rowptr[r + 1]; k += G) acc = fma(__ldcs(val + k), __ldg(x + __ldcs(colidx + k)), acc);
+  if (r < n) {
+    const int64_t e = rowptr[r + 1];
+    int64_t k = rowptr[r] + sub;
+    for (; k + 3 * G < e; k += 4 * G) {  // four independent loads in flight per lane
+      const double v0 = __ldcs(val + k), v1 = __ldcs(val + k + G), v2 = __ldcs(val + k + 2 * G), v3 = __ldcs(val + k + 3 * G);
+      const int32_t c0 = __ldcs(colidx + k), c1 = __ldcs(colidx + k + G), c2 = __ldcs(colidx + k + 2 * G),
+                    c3 = __ldcs(colidx + k + 3 * G);
+      acc = fma(v0, __ldg(x + c0), acc);
+      acc = fma(v1, __ldg(x + c1), acc);
+      acc = fma(v2, __ldg(x + c2), acc);
+      acc = fma(v3, __ldg(x + c3), acc);
+    }
+    for (; k < e; k += G) acc = fma(__ldcs(val + k), __ldg(x + __ldcs(colidx + k)), acc);
+  }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
   return acc;
@@ -188,6 +201,13 @@ __global__ void __launch_bounds__(SV_THREADS) k_cg_init(int64_t n, const int64_t
   }
 }
 
+// lanes per CSR row of the SpMV kernels (FEM_SPMV_LANES = 8 | 16 | 32 for A/B runs)
+static int spmv_lanes() {
+  const char* e = getenv("FEM_SPMV_LANES");
+  const int g = e ? atoi(e) : 32;  // c5: 32 lanes 12.8 ms, 16 lanes 13.8 ms, 8 lanes 14.6 ms per SpMV
+  return (g == 16 || g == 32) ? g : 8;
+}
+
 static int grid_for(int64_t n, int per_thread_rows) {
   const int64_t need = (n * per_thread_rows + SV_THREADS - 1) / SV_THREADS;
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, SV_MAX_BLOCKS));
@@ -204,7 +224,10 @@ extern "C" int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* co
     return FEM_E_INVALID_ARG;
   }
   if (n_rows == 0) return 0;
-  k_spmv<8><<<grid_for(n_rows, 8), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  const int g = spmv_lanes();
+  if (g == 32) k_spmv<32><<<grid_for(n_rows, 32), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  else if (g == 16) k_spmv<16><<<grid_for(n_rows, 16), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  else k_spmv<8><<<grid_for(n_rows, 8), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -232,7 +255,8 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
   CgScal* sc = reinterpret_cast<CgScal*>(partials + 2 * SV_MAX_BLOCKS);
   int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(CgScal));
   FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(CgScal) + 8, s));
-  const int gv = grid_for(n, 1), gm = grid_for(n, 8);
+  const int g = spmv_lanes();
+  const int gv = grid_for(n, 1), gm = grid_for(n, g);
   k_cg_init<<<gv, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, b, x, r, z, dinv, partials, sc, bad);
   k_cg_dir<<<gv, SV_THREADS, 0, s>>>(n, z, p, sc, 1);
   FEM_CUDA_TRY(cudaGetLastError());
@@ -252,7 +276,9 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
   while (rr0 > 0.0 && it < max_iter && rel > rtol) {
     const int todo = std::min(chk, max_iter - it);
     for (int k = 0; k < todo; k++) {
-      k_cg_spmv<8><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
+      if (g == 32) k_cg_spmv<32><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
+      else if (g == 16) k_cg_spmv<16><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
+      else k_cg_spmv<8><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
       k_cg_update<<<gv, SV_THREADS, 0, s>>>(n, x, r, p, q, dinv, z, partials, sc);
       k_cg_dir<<<gv, SV_THREADS, 0, s>>>(n, z, p, sc, 0);
     }
