@@ -35,6 +35,7 @@ extern "C" {
 #define FEM_E_UNSUPPORTED (-2)      /* element/order/quadrature/form combination not built      */
 #define FEM_E_INDEX_OVERFLOW (-3)   /* a count exceeds the index width (int32 columns/slots)      */
 #define FEM_E_INVERTED_ELEMENT (-4) /* det J <= 0 at some quadrature point                */
+#define FEM_E_NAN (-5)              /* a NaN / breakdown in an iterative solve             */
 #define FEM_E_CUDA (-6)
 #define FEM_E_OOM (-8)
 
@@ -199,6 +200,15 @@ int fem_pattern_info(fem_pattern_t pat, int64_t* out8);
  *   read-only): rowptr int64 [n_rows+1], colidx int32 [nnz] (global column ids; *col_offset = own_lo, 0
  *   on a single GPU).  No copy, no sync. */
 int fem_pattern_csr(fem_pattern_t pat, const int64_t** rowptr, const int32_t** colidx, int64_t* col_offset);
+/* fem_bicgstab_solve — Jacobi-preconditioned BiCGStab for K x = b with a non-symmetric K (the thermal FIX
+ *   term k N_a n·∇T, and the NS forms make K non-symmetric).  Same conventions as
+ *   fem_cg_solve (DEVICE vectors, caller-owned work of fem_bicgstab_work_doubles(n_rows) doubles, host
+ *   syncs every check_every iterations, fixed-order reductions).  FEM_E_INVALID_ARG for a zero diagonal;
+ *   FEM_E_NAN on breakdown. */
+int64_t fem_bicgstab_work_doubles(int64_t n_rows);
+int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+                       const double* b, double* x, int max_iter, double rtol, int check_every, double* work,
+                       int* iters_out, double* relres_out, void* stream);
 int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
              const double* x, double* y, double alpha, double beta, void* stream);
 int64_t fem_cg_work_doubles(int64_t n_rows);

@@ -201,6 +201,134 @@ __global__ void __launch_bounds__(SV_THREADS) k_cg_init(int64_t n, const int64_t
   }
 }
 
+// ---- Jacobi-preconditioned BiCGStab (van der Vorst) for the non-symmetric systems: the thermal FIX term
+// k N_a n·∇T and the NS forms make K non-symmetric, so CG does not apply.
+// Vectors in the work buffer: r, rh (shadow residual), p, v, y, s, z, t, dinv; scalars in BiScal.
+struct BiScal {
+  double rho, rho_new, alpha, omega, rv, ts, tt, rr, rr0;
+  unsigned int count0, count1;
+};
+
+// p = r + β (p - ω v), β = (ρ_new / ρ)(α / ω); y = D^-1 p   (first: p = r)
+__global__ void __launch_bounds__(SV_THREADS) k_bi_dir(int64_t n, const double* __restrict__ r, double* __restrict__ p,
+                                                       const double* __restrict__ v, const double* __restrict__ dinv,
+                                                       double* __restrict__ y, const BiScal* sc, int first) {
+  // breakdown guards (ρ = 0 or ω = 0): restart the direction from r instead of propagating NaN
+  const bool restart = first || sc->rho == 0.0 || sc->omega == 0.0;
+  const double beta = restart ? 0.0 : (sc->rho_new / sc->rho) * (sc->alpha / sc->omega), om = sc->omega;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS) {
+    const double pi = restart ? r[i] : fma(beta, p[i] - om * v[i], r[i]);
+    p[i] = pi;
+    y[i] = dinv[i] * pi;
+  }
+}
+
+// out = A in (A = K), and (a · out) [, (out · out)] reduced; the last block forms α or ω
+template <int G, int MODE>  // MODE 0: v = A y, α = ρ_new / (rh·v);  MODE 1: t = A z, ω = (t·s)/(t·t)
+__global__ void __launch_bounds__(SV_THREADS) k_bi_spmv(int64_t n, const int64_t* __restrict__ rowptr,
+                                                        const int32_t* __restrict__ colidx,
+                                                        const double* __restrict__ val, const double* __restrict__ in,
+                                                        double* __restrict__ out, const double* __restrict__ a,
+                                                        double* partials, BiScal* sc) {
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31, sub = lane % G;
+  const int64_t nwarps = (int64_t)gridDim.x * (SV_THREADS / 32);
+  double d0 = 0.0, d1 = 0.0;
+  for (int64_t w = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) / 32; w * RPW < n; w += nwarps) {
+    const int64_t r = w * RPW + lane / G;
+    const double acc = row_dot<G>(r, n, sub, rowptr, colidx, val, in);
+    if (sub == 0 && r < n) {
+      out[r] = acc;
+      d0 = fma(a[r], acc, d0);
+      if (MODE == 1) d1 = fma(acc, acc, d1);
+    }
+  }
+  double o;
+  if (block_reduce_last(d0, partials, &sc->count0, &o)) {
+    if (MODE == 0) {
+      sc->rv = o;
+      sc->rho = sc->rho_new;  // k_bi_dir of this iteration has used the old ρ (stream order)
+      sc->alpha = o != 0.0 ? sc->rho / o : 0.0;
+    } else {
+      sc->ts = o;
+    }
+  }
+  if (MODE == 1) {
+    __syncthreads();
+    if (block_reduce_last(d1, partials + gridDim.x, &sc->count1, &o)) {
+      sc->tt = o;
+      sc->omega = o != 0.0 ? sc->ts / o : 0.0;
+    }
+  }
+}
+
+// x += α y; s = r - α v; z = D^-1 s
+__global__ void __launch_bounds__(SV_THREADS) k_bi_half(int64_t n, double* __restrict__ x, const double* __restrict__ y,
+                                                        const double* __restrict__ r, const double* __restrict__ v,
+                                                        const double* __restrict__ dinv, double* __restrict__ sv,
+                                                        double* __restrict__ z, const BiScal* sc) {
+  const double al = sc->alpha;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS) {
+    x[i] = fma(al, y[i], x[i]);
+    const double si = fma(-al, v[i], r[i]);
+    sv[i] = si;
+    z[i] = dinv[i] * si;
+  }
+}
+
+// x += ω z; r = s - ω t; ρ_new = rh·r, rr = r·r
+__global__ void __launch_bounds__(SV_THREADS) k_bi_fin(int64_t n, double* __restrict__ x, const double* __restrict__ z,
+                                                       const double* __restrict__ sv, const double* __restrict__ t,
+                                                       const double* __restrict__ rh, double* __restrict__ r,
+                                                       double* partials, BiScal* sc) {
+  const double om = sc->omega;
+  double d0 = 0.0, d1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS) {
+    x[i] = fma(om, z[i], x[i]);
+    const double ri = fma(-om, t[i], sv[i]);
+    r[i] = ri;
+    d0 = fma(rh[i], ri, d0);
+    d1 = fma(ri, ri, d1);
+  }
+  double o;
+  if (block_reduce_last(d0, partials, &sc->count0, &o)) sc->rho_new = o;
+  __syncthreads();
+  if (block_reduce_last(d1, partials + gridDim.x, &sc->count1, &o)) sc->rr = o;
+}
+
+// r = b - A x, rh = r, dinv = 1 / diag(A) (non-zero diagonal required), ρ_new = r·r = rr0
+__global__ void __launch_bounds__(SV_THREADS) k_bi_init(int64_t n, const int64_t* __restrict__ rowptr,
+                                                        const int32_t* __restrict__ colidx,
+                                                        const double* __restrict__ val, const double* __restrict__ b,
+                                                        const double* __restrict__ x, double* __restrict__ r,
+                                                        double* __restrict__ rh, double* __restrict__ dinv,
+                                                        double* partials, BiScal* sc, int* bad_diag) {
+  double d0 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS) {
+    double ax = 0.0, dg = 0.0;
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; k++) {
+      const int32_t c = colidx[k];
+      ax = fma(val[k], x[c], ax);
+      if (c == i) dg = val[k];
+    }
+    if (dg == 0.0) atomicExch(bad_diag, 1);
+    dinv[i] = 1.0 / dg;
+    const double ri = b[i] - ax;
+    r[i] = ri;
+    rh[i] = ri;
+    d0 = fma(ri, ri, d0);
+  }
+  double o;
+  if (block_reduce_last(d0, partials, &sc->count0, &o)) {
+    sc->rho_new = o;
+    sc->rr = o;
+    sc->rr0 = o;
+    sc->rho = 1.0;
+    sc->alpha = 1.0;
+    sc->omega = 1.0;
+  }
+}
+
 // lanes per CSR row of the SpMV kernels (FEM_SPMV_LANES = 8 | 16 | 32 for A/B runs)
 static int spmv_lanes() {
   const char* e = getenv("FEM_SPMV_LANES");
@@ -287,6 +415,80 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
     FEM_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof(CgScal), cudaMemcpyDeviceToHost, s));
     FEM_CUDA_TRY(cudaStreamSynchronize(s));
     rel = sqrt(h.rr / rr0);
+  }
+  if (iters_out) *iters_out = it;
+  if (relres_out) *relres_out = rel;
+  return 0;
+}
+
+extern "C" int64_t fem_bicgstab_work_doubles(int64_t n_rows) {
+  return 9 * n_rows + 2 * SV_MAX_BLOCKS + (int64_t)(sizeof(BiScal) + 7) / 8 + 8;
+}
+
+extern "C" int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+                                  const double* b, double* x, int max_iter, double rtol, int check_every, double* work,
+                                  int* iters_out, double* relres_out, void* stream) {
+  if (n_rows <= 0 || !rowptr || !colidx || !values || !b || !x || !work || max_iter < 0 || !(rtol >= 0.0)) {
+    set_error("fem_bicgstab_solve: invalid argument (n_rows > 0, non-NULL pointers, rtol >= 0)");
+    return FEM_E_INVALID_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = n_rows;
+  double* r = work;
+  double* rh = r + n;
+  double* p = rh + n;
+  double* v = p + n;
+  double* y = v + n;
+  double* sv = y + n;
+  double* z = sv + n;
+  double* t = z + n;
+  double* dinv = t + n;
+  double* partials = dinv + n;
+  BiScal* sc = reinterpret_cast<BiScal*>(partials + 2 * SV_MAX_BLOCKS);
+  int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(BiScal));
+  FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(BiScal) + 8, st));
+  const int g = spmv_lanes();
+  const int gv = grid_for(n, 1), gm = grid_for(n, g);
+  k_bi_init<<<gv, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, b, x, r, rh, dinv, partials, sc, bad);
+  FEM_CUDA_TRY(cudaGetLastError());
+  BiScal h{};
+  int hbad = 0;
+  FEM_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof(BiScal), cudaMemcpyDeviceToHost, st));
+  FEM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FEM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hbad) {
+    set_error("fem_bicgstab_solve: zero diagonal entry (Jacobi preconditioner undefined)");
+    return FEM_E_INVALID_ARG;
+  }
+  const double rr0 = h.rr0;
+  int it = 0;
+  double rel = rr0 > 0.0 ? 1.0 : 0.0;
+  const int chk = check_every > 0 ? check_every : 16;
+  while (rr0 > 0.0 && it < max_iter && rel > rtol) {
+    const int todo = std::min(chk, max_iter - it);
+    for (int k = 0; k < todo; k++) {
+      k_bi_dir<<<gv, SV_THREADS, 0, st>>>(n, r, p, v, dinv, y, sc, it + k == 0);
+#define BI_SPMV(MODE, IN, OUT, A)                                                                                 \
+  if (g == 32) k_bi_spmv<32, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
+  else if (g == 16) k_bi_spmv<16, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
+  else k_bi_spmv<8, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc);
+      BI_SPMV(0, y, v, rh)
+      k_bi_half<<<gv, SV_THREADS, 0, st>>>(n, x, y, r, v, dinv, sv, z, sc);
+      BI_SPMV(1, z, t, sv)
+#undef BI_SPMV
+      k_bi_fin<<<gv, SV_THREADS, 0, st>>>(n, x, z, sv, t, rh, r, partials, sc);
+    }
+    FEM_CUDA_TRY(cudaGetLastError());
+    it += todo;
+    FEM_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof(BiScal), cudaMemcpyDeviceToHost, st));
+    FEM_CUDA_TRY(cudaStreamSynchronize(st));
+    rel = sqrt(h.rr / rr0);
+    if (!(rel == rel)) {
+      set_error("fem_bicgstab_solve: breakdown (NaN in the recurrence)");
+      if (iters_out) *iters_out = it;
+      if (relres_out) *relres_out = rel;
+      return FEM_E_NAN;
+    }
   }
   if (iters_out) *iters_out = it;
   if (relres_out) *relres_out = rel;

@@ -25,7 +25,7 @@ FORM = {
     "ELAST_DOMAIN": 3, "ELAST_FIX_ALL": 4, "ELAST_FIX_D1": 5, "ELAST_LOAD": 6,
     "NS_DOMAIN": 7, "NS_BND_INFLOW": 8, "NS_BND_OUTFLOW": 9, "NS_BND_FIX": 10,
 }
-ERRORS = {-1: "INVALID_ARG", -2: "UNSUPPORTED", -3: "INDEX_OVERFLOW", -4: "INVERTED_ELEMENT",
+ERRORS = {-1: "INVALID_ARG", -2: "UNSUPPORTED", -3: "INDEX_OVERFLOW", -4: "INVERTED_ELEMENT", -5: "NAN",
           -6: "CUDA", -8: "OOM"}
 
 
@@ -132,6 +132,10 @@ def lib():
         L.fem_cg_work_doubles.restype = I64
         L.fem_cg_solve.argtypes = [I64, V, V, V, V, V, C.c_double, I, C.c_double, I, V, C.POINTER(I),
                                    C.POINTER(C.c_double), V]
+        L.fem_bicgstab_work_doubles.argtypes = [I64]
+        L.fem_bicgstab_work_doubles.restype = I64
+        L.fem_bicgstab_solve.argtypes = [I64, V, V, V, V, V, I, C.c_double, I, V, C.POINTER(I),
+                                         C.POINTER(C.c_double), V]
         L.fem_last_error.restype = C.c_char_p
         L.fem_version.restype = I
         _lib = L
@@ -142,7 +146,7 @@ EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pa
             "fem_assemble_matrix", "fem_assemble_residual", "fem_assemble_system", "fem_residual_norms",
             "fem_linearize_host", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
-            "fem_cg_work_doubles", "fem_cg_solve"]
+            "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve"]
 
 
 def _check(rc):
@@ -272,6 +276,20 @@ def fem_cg_solve(n_rows, rowptr, colidx, values, b, x, work, spd_sign=-1.0, max_
     _check(lib().fem_cg_solve(int(n_rows), _ptr(rowptr), _ptr(colidx), _ptr(values), _ptr(b), _ptr(x),
                               float(spd_sign), int(max_iter), float(rtol), int(check_every), _ptr(work),
                               C.byref(it), C.byref(rel), _stream(stream)))
+    return it.value, rel.value
+
+
+def fem_bicgstab_work_doubles(n_rows):
+    return int(lib().fem_bicgstab_work_doubles(int(n_rows)))
+
+
+def fem_bicgstab_solve(n_rows, rowptr, colidx, values, b, x, work, max_iter=10000, rtol=1e-12, check_every=16,
+                       stream=None):
+    """Jacobi-BiCGStab for K x = b (non-symmetric K); returns (iterations, ||r||/||r0||)."""
+    it, rel = C.c_int(0), C.c_double(0.0)
+    _check(lib().fem_bicgstab_solve(int(n_rows), _ptr(rowptr), _ptr(colidx), _ptr(values), _ptr(b), _ptr(x),
+                                    int(max_iter), float(rtol), int(check_every), _ptr(work), C.byref(it),
+                                    C.byref(rel), _stream(stream)))
     return it.value, rel.value
 
 

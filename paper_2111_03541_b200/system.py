@@ -77,19 +77,30 @@ class FemSystem:
         return self.values, self.rhs
 
     # ---- NEXT-1: the Newton sub-step's linear solve (D-4) on the GPU
-    def solve(self, b, x=None, spd_sign=-1.0, rtol=1e-12, max_iter=20000, check_every=16):
-        """Solve K x = b for the last assembled K (self.values) with Jacobi-PCG on (spd_sign K) — the
-        thermal / elasticity K is negative definite in the paper's sign convention (reading L17).
-        Returns (x, iterations, ||r|| / ||r0||).  Single-GPU patterns only."""
+    def solve(self, b, x=None, spd_sign=-1.0, rtol=1e-12, max_iter=20000, check_every=16, method="cg"):
+        """Solve K x = b for the last assembled K (self.values).  method "cg": Jacobi-PCG on (spd_sign K)
+        — the elasticity K is symmetric negative definite in the paper's sign convention (reading L17);
+        "bicgstab": Jacobi-BiCGStab for non-symmetric K (thermal FIX, NS).  Returns (x, iterations,
+        ||r|| / ||r0||).  Single-GPU patterns only."""
         if self.own != (0, self.N):
-            raise ValueError("solve: the CG solver takes a single-GPU (unpartitioned) pattern")
+            raise ValueError("solve: the iterative solvers take a single-GPU (unpartitioned) pattern")
         if x is None:
             x = torch.zeros(self.n_rows, dtype=torch.float64, device=self.device)
-        if getattr(self, "_cg_work", None) is None:
-            self._cg_work = torch.empty(fem.fem_cg_work_doubles(self.n_rows), dtype=torch.float64, device=self.device)
         rp, ci, _ = fem.fem_pattern_csr(self.pat_h)
-        it, rel = fem.fem_cg_solve(self.n_rows, rp, ci, self.values, b, x, self._cg_work, spd_sign, max_iter, rtol,
-                                   check_every)
+        if method == "cg":
+            if getattr(self, "_cg_work", None) is None:
+                self._cg_work = torch.empty(fem.fem_cg_work_doubles(self.n_rows), dtype=torch.float64,
+                                            device=self.device)
+            it, rel = fem.fem_cg_solve(self.n_rows, rp, ci, self.values, b, x, self._cg_work, spd_sign, max_iter,
+                                       rtol, check_every)
+        elif method == "bicgstab":
+            if getattr(self, "_bi_work", None) is None:
+                self._bi_work = torch.empty(fem.fem_bicgstab_work_doubles(self.n_rows), dtype=torch.float64,
+                                            device=self.device)
+            it, rel = fem.fem_bicgstab_solve(self.n_rows, rp, ci, self.values, b, x, self._bi_work, max_iter, rtol,
+                                             check_every)
+        else:
+            raise ValueError(method)
         return x, it, rel
 
     def spmv(self, x, y=None, alpha=1.0, beta=0.0):
@@ -100,11 +111,11 @@ class FemSystem:
         fem.fem_spmv(self.n_rows, rp, ci, self.values, x, y, alpha, beta)
         return y
 
-    def newton_step(self, state, scatter="tiled", spd_sign=-1.0, rtol=1e-12, max_iter=20000):
+    def newton_step(self, state, scatter="tiled", spd_sign=-1.0, rtol=1e-12, max_iter=20000, method="cg"):
         """One Newton sub-step (D-1..D-4) for a static problem: assemble K and d at φ, solve
-        K Δφ = -d, return φ + Δφ (state level 0), the CG iterations and relative residual."""
+        K Δφ = -d, return φ + Δφ (state level 0), the solver iterations and relative residual."""
         K, d = self.system(state, scatter=scatter)
-        dx, it, rel = self.solve(-d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter)
+        dx, it, rel = self.solve(-d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method)
         new = state.clone()
         new[0] += dx.view(self.kh, self.N)
         return new, it, rel

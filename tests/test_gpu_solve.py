@@ -111,3 +111,72 @@ def test_cantilever_tip_deflection_matches_beam_theory():
     timoshenko = P * L ** 3 / (3 * E * I) + P * L / (kappa * G * A)
     assert abs(-uy[tip].mean() / timoshenko - 1.0) <= 5e-3
     S.close()
+
+
+@pytest.mark.parametrize("name,dims", [("c1", (8,)), ("c2", (9, 7, 6))])
+def test_bicgstab_matches_direct_solve_nonsymmetric(name, dims):
+    """The thermal FIX term k N_a n·∇T makes K non-symmetric: BiCGStab.  (The NS saddle-point
+    system, diverges under a Jacobi preconditioner; it needs a block preconditioner — DESIGN.)"""
+    _need_gpu()
+    import scipy.sparse.linalg as spla
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config(name, "perturbed", dims)
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    K = _csr(ora)
+    assert abs(K - K.T).max() > 0  # really non-symmetric
+    x_ref = spla.spsolve(K.tocsc(), -ora["rhs"])
+    S = FemSystem(m, p)
+    _, dg = S.system(torch.from_numpy(st).cuda(), scatter="tiled")
+    x, it, rel = S.solve(-dg, rtol=1e-13, max_iter=200000, method="bicgstab")
+    assert rel <= 1e-13
+    x = x.cpu().numpy()
+    assert np.linalg.norm(K @ x + ora["rhs"]) / np.linalg.norm(ora["rhs"]) <= 1e-11
+    kappa = np.linalg.cond(K.toarray())
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 10 * kappa * 1e-13
+    x2, it2, rel2 = S.solve(-dg, rtol=1e-13, max_iter=200000, method="bicgstab")
+    assert it2 == it and np.array_equal(x2.cpu().numpy(), x)
+    S.close()
+
+
+def _gpu_manufactured_error(n, etype):
+    """The oracle pin's manufactured problem (T* = Π sin πx_d, s = dim π² T*, penalty 1e8·k/h, reading L22),
+    assembled and solved on the GPU (one Newton step from T = 0, BiCGStab); the L2 error by quadrature."""
+    import math
+    from fem_inputs.meshgen import facets_on_plane, hex_box, tri_square
+    from helpers import problem
+    from paper_2111_03541_b200 import FemSystem
+    if etype == "tri":
+        m = tri_square(n)
+        be = [facets_on_plane(m, a, v) for a in (0, 1) for v in (0.0, 1.0)]
+        s, dim = 2 * math.pi ** 2, 2
+    else:
+        m = hex_box(n, n, n)
+        be = [facets_on_plane(m, a, v) for a in (0, 1, 2) for v in (0.0, 1.0)]
+        s, dim = 3 * math.pi ** 2, 3
+    m.bsets = [(np.concatenate([b[0] for b in be]), np.concatenate([b[1] for b in be]))]
+    pr = problem("thermal", etype, 1, [("THERMAL_DOMAIN", -1, dict(C=0.0, k=1.0, s=s, source="sine")),
+                                       ("THERMAL_FIX", 0, dict(h_p=1e8 * n, T_fix=0.0, k=1.0))])
+    S = FemSystem(m, pr)
+    st = torch.zeros((1, 1, m.n_nodes), dtype=torch.float64, device="cuda")
+    st1, it, rel = S.newton_step(st, scatter="tiled", rtol=1e-12, max_iter=500000, method="bicgstab")
+    assert rel <= 1e-12
+    T = st1[0, 0].cpu().numpy()
+    S.close()
+    err2 = 0.0
+    for e in range(m.n_elems):
+        d = oracle.qp_data(m, pr, e)
+        Th = d["N"] @ T[m.conn[:, e]]
+        ex = np.prod(np.sin(np.pi * d["x"][:, :dim]), axis=1)
+        err2 += (d["w"] * (Th - ex) ** 2).sum()
+    return math.sqrt(err2)
+
+
+@pytest.mark.parametrize("etype,ns", [("tri", (8, 16, 32, 64)), ("hex", (4, 8, 16))])
+def test_gpu_manufactured_convergence_rate(etype, ns):
+    """The whole GPU path (assembly + solve) against mathematics: P1 / Q1 L2 error rate -> 2."""
+    _need_gpu()
+    import math
+    errs = [_gpu_manufactured_error(n, etype) for n in ns]
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+    assert all(1.8 < r < 2.3 for r in rates), (errs, rates)
