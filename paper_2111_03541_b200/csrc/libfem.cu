@@ -3,6 +3,7 @@
 // (P:343-465); readings in DESIGN.md §4.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -316,18 +317,36 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
   int rc = check_problem(m, prob);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  bool bnd_only = false;  // tiled NS: domain terms in the tile kernel, boundary terms coloured afterwards
   if (scatter == FEM_SCATTER_TILED) {
     if (accumulate) { set_error("tiled scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
     if (!p) { set_error("tiled scatter needs the pattern"); return FEM_E_INVALID_ARG; }
-    return launch_tiled(m, p, prob, state, values, rhs, s);
-  }
-  if (scatter != FEM_SCATTER_ATOMIC && scatter != FEM_SCATTER_COLOURED) { set_error("bad scatter mode"); return FEM_E_INVALID_ARG; }
-  if (!accumulate) {  // "cleared first" (D-2 P:426, D-3 P:441)
+    // NS on P1 tets: the generic boundary terms (1% of the visits) would stall the whole tile
+    // behind a facet phase run by a few warps (22% of c4); they run instead as the deterministic coloured
+    // facet pass over the rows the tile kernel has written (FEM_NS_FACET_PHASE=1 keeps the in-tile phase)
+    const bool ns_split = m->etype == FEM_TET && m->order == 1 && m->physics == FEM_NS && !getenv("FEM_NS_FACET_PHASE");
+    if (!ns_split) return launch_tiled(m, p, prob, state, values, rhs, s);
+    fem_problem dom = *prob;
+    dom.n_terms = 0;
+    bool any_bnd = false;
+    for (int t = 0; t < prob->n_terms; t++) {
+      if (prob->terms[t].region < 0) dom.terms[dom.n_terms++] = prob->terms[t];
+      else any_bnd = true;
+    }
+    rc = launch_tiled(m, p, &dom, state, values, rhs, s);
+    if (rc || !any_bnd) return rc;
+    bnd_only = true;
+    scatter = FEM_SCATTER_COLOURED;
+  } else if (scatter != FEM_SCATTER_ATOMIC && scatter != FEM_SCATTER_COLOURED) {
+    set_error("bad scatter mode");
+    return FEM_E_INVALID_ARG;
+  } else if (!accumulate) {  // "cleared first" (D-2 P:426, D-3 P:441)
     if (values) FEM_CUDA_TRY(cudaMemsetAsync(values, 0, sizeof(double) * p->nnz, s));
     if (rhs) FEM_CUDA_TRY(cudaMemsetAsync(rhs, 0, sizeof(double) * m->kh * m->n_own, s));
   }
   for (int t = 0; t < prob->n_terms; t++) {
     const fem_term& T = prob->terms[t];
+    if (bnd_only && T.region < 0) continue;
     AsmArgs A;
     A.m = m; A.pat = p; A.F = make_form_args(prob, T); A.quad_order = prob->quad_order; A.state = state;
     A.values = (T.form == FEM_WF_ELAST_LOAD) ? nullptr : values;

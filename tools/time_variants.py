@@ -1,14 +1,15 @@
-"""Dev A/B: time the c5 tiled system call with and without its boundary terms (facet phase cost).
-python tools/time_variants.py [dims...]"""
+"""Dev A/B: time a config's tiled system call with and without its boundary terms (facet phase cost).
+python tools/time_variants.py [config] [dims...]"""
 import sys
 import torch
 sys.path.insert(0, '.')
 from fem_inputs import make_config, make_state
 from paper_2111_03541_b200 import FemSystem
 
-dims = tuple(int(x) for x in sys.argv[1:]) or None
-m, p = make_config('c5', 'structured', dims)
-st = torch.from_numpy(make_state('c5', m, p)).cuda()
+name = sys.argv[1] if len(sys.argv) > 1 else 'c5'
+dims = tuple(int(x) for x in sys.argv[2:]) or None
+m, p = make_config(name, 'structured', dims)
+st = torch.from_numpy(make_state(name, m, p)).cuda()
 for label, terms in [('all terms', p.terms), ('domain only', p.terms[:1])]:
     p.terms = terms
     S = FemSystem(m, p)
