@@ -318,6 +318,14 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   bool bnd_only = false;  // tiled NS: domain terms in the tile kernel, boundary terms coloured afterwards
+  if (scatter == FEM_SCATTER_TILED && !values && m->etype == FEM_TET && !getenv("FEM_NS_DET") &&
+      !getenv("FEM_TILED_RESIDUAL")) {
+    // residual-only on tets: the tile kernels visit each element ~3x (24 elements per vertex) and their
+    // shared-memory sums are atomic (not ordered) anyway, so the element pass with fp64 RED into the
+    // (L2-sized) rhs is the faster unordered path (c3 3.0 -> 0.9 ms, c4 25 -> 12.5 ms)
+    scatter = FEM_SCATTER_ATOMIC;
+    accumulate = 0;
+  }
   if (scatter == FEM_SCATTER_TILED) {
     if (accumulate) { set_error("tiled scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
     if (!p) { set_error("tiled scatter needs the pattern"); return FEM_E_INVALID_ARG; }
