@@ -33,8 +33,11 @@ def _csr(ora):
 
 
 @pytest.mark.parametrize("name,dims", [("c1", (8,)), ("c3", (7, 3, 2)), ("c4", (9, 4, 3)), ("c5", (7, 5, 6))])
-def test_spmv_matches_scipy_on_oracle_matrix(name, dims):
+@pytest.mark.parametrize("spmv", ["row", "tma"])
+def test_spmv_matches_scipy_on_oracle_matrix(name, dims, spmv, monkeypatch):
     _need_gpu()
+    if spmv == "tma":
+        monkeypatch.setenv("FEM_SPMV_TMA", "1")
     from paper_2111_03541_b200 import FemSystem
     m, p = make_config(name, "perturbed", dims)
     st = make_state(name, m, p)
@@ -54,8 +57,11 @@ def test_spmv_matches_scipy_on_oracle_matrix(name, dims):
 
 
 @pytest.mark.parametrize("name,dims", [("c5", (7, 5, 6)), ("c3", (7, 3, 2))])
-def test_cg_matches_direct_solve_and_is_bit_reproducible(name, dims):
+@pytest.mark.parametrize("spmv", ["row", "tma"])
+def test_cg_matches_direct_solve_and_is_bit_reproducible(name, dims, spmv, monkeypatch):
     _need_gpu()
+    if spmv == "tma":  # the TMA-staged SpMV variant (read at launch)
+        monkeypatch.setenv("FEM_SPMV_TMA", "1")
     import scipy.sparse.linalg as spla
     from paper_2111_03541_b200 import FemSystem
     m, p = make_config(name, "perturbed", dims)
