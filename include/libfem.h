@@ -166,6 +166,15 @@ int fem_linearize_host(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* pr
                        const double* state_host, double* values, double* rhs, double* norms_host,
                        int scatter, void* stream);
 
+/* fem_linearize_host_async — fem_linearize_host without the final synchronization, pipelined: the state
+ * is staged through two library-owned device buffers on a library-owned copy stream, so the host->device
+ * copy of this call overlaps the assembly of the previous call on `stream`.  norms_host (pinned) is
+ * valid, and state_host may be modified, once `stream` has completed this call's work (the caller syncs).
+ * values / rhs are overwritten by every call in stream order. */
+int fem_linearize_host_async(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* prob,
+                             const double* state_host, double* values, double* rhs, double* norms_host,
+                             int scatter, void* stream);
+
 /* fem_get_status — synchronizes `stream`; returns 0 or FEM_E_INVERTED_ELEMENT (bad_elem = an
  * offending element id, else -1).  Resets the device error word. */
 int fem_get_status(fem_mesh_t mesh, void* stream, int64_t* bad_elem);

@@ -132,6 +132,12 @@ struct fem_mesh_s {
   long long* err = nullptr;     // device error word: an offending element id or -1
   double* scratch_state = nullptr;  // e2e staging buffer (lazily allocated)
   size_t scratch_state_bytes = 0;
+  // pipelined e2e (fem_linearize_host_async): two staging buffers, a copy stream and their events
+  double* async_state[2] = {nullptr, nullptr};
+  size_t async_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  int64_t async_calls = 0;
   int n_colours = 0;
   int64_t last_n_tiles = 0;
 };

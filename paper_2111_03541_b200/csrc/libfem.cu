@@ -108,6 +108,12 @@ void fem_mesh_destroy(fem_mesh_t m) {
   for (auto p : m->bset_facet_dev) cudaFree(p);
   cudaFree(m->err);
   if (m->scratch_state) cudaFree(m->scratch_state);
+  for (int b = 0; b < 2; b++) {
+    if (m->async_state[b]) cudaFree(m->async_state[b]);
+    if (m->ev_copied[b]) cudaEventDestroy(m->ev_copied[b]);
+    if (m->ev_used[b]) cudaEventDestroy(m->ev_used[b]);
+  }
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
   delete m;
 }
 
@@ -429,6 +435,52 @@ int fem_linearize_host(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, c
   if (rc) return rc;
   FEM_CUDA_TRY(cudaMemcpyAsync(norms_host, nd, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   FEM_CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fem_linearize_host_async(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, const double* state_host,
+                             double* values, double* rhs, double* norms_host, int scatter, void* stream) {
+  if (!m || !p || !prob || !state_host || !values || !rhs || !norms_host) {
+    set_error("fem_linearize_host_async: NULL argument");
+    return FEM_E_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int levels = (prob->time.kind == FEM_TIME_GENALPHA ? prob->time.nu_hat : 0) + 1;
+  const size_t bytes = sizeof(double) * levels * m->kh * m->N;
+  if (!m->copy_stream) {
+    FEM_CUDA_TRY(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; b++) {
+      FEM_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_copied[b], cudaEventDisableTiming));
+      FEM_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_used[b], cudaEventDisableTiming));
+    }
+  }
+  if (m->async_bytes < bytes + 2 * sizeof(double)) {
+    FEM_CUDA_TRY(cudaStreamSynchronize(s));
+    FEM_CUDA_TRY(cudaStreamSynchronize(m->copy_stream));
+    for (int b = 0; b < 2; b++) {
+      if (m->async_state[b]) cudaFree(m->async_state[b]);
+      m->async_state[b] = nullptr;
+    }
+    m->async_bytes = 0;
+    for (int b = 0; b < 2; b++) FEM_CUDA_TRY(cudaMalloc(&m->async_state[b], bytes + 2 * sizeof(double)));
+    m->async_bytes = bytes + 2 * sizeof(double);
+    m->async_calls = 0;
+  }
+  const int b = (int)(m->async_calls & 1);
+  // the staging buffer b was last read by the assembly of call k-2: the copy waits for it, then this
+  // call's H2D runs on the copy stream while the previous call's assembly runs on `stream`
+  if (m->async_calls >= 2) FEM_CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, m->ev_used[b], 0));
+  FEM_CUDA_TRY(cudaMemcpyAsync(m->async_state[b], state_host, bytes, cudaMemcpyHostToDevice, m->copy_stream));
+  FEM_CUDA_TRY(cudaEventRecord(m->ev_copied[b], m->copy_stream));
+  FEM_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_copied[b], 0));
+  int rc = assemble(m, p, prob, m->async_state[b], values, rhs, 0, scatter, stream);
+  if (rc) return rc;
+  double* nd = m->async_state[b] + levels * m->kh * m->N;
+  rc = residual_norms(m, rhs, nd, s);
+  if (rc) return rc;
+  FEM_CUDA_TRY(cudaMemcpyAsync(norms_host, nd, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA_TRY(cudaEventRecord(m->ev_used[b], s));
+  m->async_calls++;
   return 0;
 }
 

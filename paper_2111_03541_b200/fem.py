@@ -120,6 +120,7 @@ def lib():
         L.fem_assemble_system.argtypes = [V, V, PP, V, V, V, I, I, V]
         L.fem_residual_norms.argtypes = [V, V, V, V]
         L.fem_linearize_host.argtypes = [V, V, PP, V, V, V, V, I, V]
+        L.fem_linearize_host_async.argtypes = [V, V, PP, V, V, V, V, I, V]
         L.fem_get_status.argtypes = [V, V, C.POINTER(I64)]
         L.fem_mesh_info.argtypes = [V, C.POINTER(I), C.POINTER(I), C.POINTER(I), C.POINTER(I64)]
         L.fem_pattern_destroy.argtypes = [V]
@@ -144,7 +145,7 @@ def lib():
 
 EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pattern_export", "fem_pattern_info",
             "fem_assemble_matrix", "fem_assemble_residual", "fem_assemble_system", "fem_residual_norms",
-            "fem_linearize_host", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
+            "fem_linearize_host", "fem_linearize_host_async", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
             "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve"]
 
@@ -291,6 +292,14 @@ def fem_bicgstab_solve(n_rows, rowptr, colidx, values, b, x, work, max_iter=1000
                                     int(max_iter), float(rtol), int(check_every), _ptr(work), C.byref(it),
                                     C.byref(rel), _stream(stream)))
     return it.value, rel.value
+
+
+def fem_linearize_host_async(mesh_h, pat_h, problem, state_host, values, rhs, norms_host, scatter="atomic",
+                             stream=None, P=None):
+    """Pipelined host-buffer linearisation (no sync): the H2D of this call overlaps the previous assembly."""
+    P = P if P is not None else make_problem(problem)
+    _check(lib().fem_linearize_host_async(mesh_h, pat_h, C.byref(P), _ptr(state_host), _ptr(values), _ptr(rhs),
+                                          _ptr(norms_host), SCATTER[scatter], _stream(stream)))
 
 
 def fem_get_status(mesh_h, stream=None):
