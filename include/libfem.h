@@ -175,6 +175,17 @@ int fem_linearize_host_async(fem_mesh_t mesh, fem_pattern_t pat, const fem_probl
                              const double* state_host, double* values, double* rhs, double* norms_host,
                              int scatter, void* stream);
 
+/* ---- NEXT-4: the paper's COO view (B-4) and workpiece offsets ------------
+ * fem_pattern_export_coo — for every entry in sparse-ID order (symbol pairs (κ₀, κ_λ) then control-point
+ *   pairs (α₁, α₂), both lexicographic, reading L4): I[id] = row_offset + κ₀ N + α₁, J[id] = row_offset +
+ *   κ_λ N + α₂ (the workpiece's n^dense, as row_offset) and csr_index[id] = the entry's position in
+ *   the CSR values.  DEVICE int64 outputs of nnz entries (any may be NULL, not all); a multi-workpiece
+ *   system passes each workpiece's arrays at its n^sp.  Stream-ordered, no sync.
+ * fem_gather — dst[i] = src[index[i]] (DEVICE), e.g. the CSR values in sparse-ID order. */
+int fem_pattern_export_coo(fem_pattern_t pat, int64_t row_offset, int64_t* I, int64_t* J, int64_t* csr_index,
+                           void* stream);
+int fem_gather(int64_t n, const int64_t* index, const double* src, double* dst, void* stream);
+
 /* fem_get_status — synchronizes `stream`; returns 0 or FEM_E_INVERTED_ELEMENT (bad_elem = an
  * offending element id, else -1).  Resets the device error word. */
 int fem_get_status(fem_mesh_t mesh, void* stream, int64_t* bad_elem);

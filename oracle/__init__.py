@@ -190,3 +190,28 @@ def to_dense(out, n_cols):
     for r in range(nr):
         K[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
     return K
+
+
+def coo_view(out, n_nodes: int, kappa_hat: int, row_offset: int = 0):
+    """The paper's COO of one workpiece (NEXT-4): B-4 numbers the global entries by the
+    sparse ID of Eq. `sparse_ID` — symbol pairs (κ₀, κ_λ) (A-3) times control-point
+    pairs (α₁, α₂) (B-1 item 4), with I = (κ₀-1)α̂ + α₁, J = (κ_λ-1)α̂ + α₂ (P:398-401, 0-based
+    here).  The paper hashes both pair sets; reading L4 fixes the order: symbol pairs lexicographic in
+    (κ₀, κ_λ), control-point pairs lexicographic in (α₁, α₂).  Built by plain loops from the oracle's
+    scalar pattern and CSR (small cases only).  row_offset = the workpiece's n^dense; a caller
+    concatenating workpieces also offsets the sparse IDs by n^sp.
+    Returns dict(I, J, values) in sparse-ID order."""
+    rps, cis = out["rowptr_s"], out["colidx_s"]
+    rp, ci, va = out["rowptr"], out["colidx"], out["values"]
+    I, J, V = [], [], []
+    for k0 in range(kappa_hat):
+        for kl in range(kappa_hat):
+            for a1 in range(n_nodes):
+                for s in range(rps[a1], rps[a1 + 1]):
+                    a2 = int(cis[s])
+                    gi, gj = k0 * n_nodes + a1, kl * n_nodes + a2
+                    row = list(ci[rp[gi]:rp[gi + 1]])
+                    V.append(va[rp[gi] + row.index(gj)])
+                    I.append(gi + row_offset)
+                    J.append(gj + row_offset)
+    return dict(I=np.array(I, np.int64), J=np.array(J, np.int64), values=np.array(V, np.float64))

@@ -121,6 +121,8 @@ def lib():
         L.fem_residual_norms.argtypes = [V, V, V, V]
         L.fem_linearize_host.argtypes = [V, V, PP, V, V, V, V, I, V]
         L.fem_linearize_host_async.argtypes = [V, V, PP, V, V, V, V, I, V]
+        L.fem_pattern_export_coo.argtypes = [V, I64, V, V, V, V]
+        L.fem_gather.argtypes = [I64, V, V, V, V]
         L.fem_get_status.argtypes = [V, V, C.POINTER(I64)]
         L.fem_mesh_info.argtypes = [V, C.POINTER(I), C.POINTER(I), C.POINTER(I), C.POINTER(I64)]
         L.fem_pattern_destroy.argtypes = [V]
@@ -145,7 +147,7 @@ def lib():
 
 EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pattern_export", "fem_pattern_info",
             "fem_assemble_matrix", "fem_assemble_residual", "fem_assemble_system", "fem_residual_norms",
-            "fem_linearize_host", "fem_linearize_host_async", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
+            "fem_linearize_host", "fem_linearize_host_async", "fem_pattern_export_coo", "fem_gather", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
             "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve"]
 
@@ -300,6 +302,14 @@ def fem_linearize_host_async(mesh_h, pat_h, problem, state_host, values, rhs, no
     P = P if P is not None else make_problem(problem)
     _check(lib().fem_linearize_host_async(mesh_h, pat_h, C.byref(P), _ptr(state_host), _ptr(values), _ptr(rhs),
                                           _ptr(norms_host), SCATTER[scatter], _stream(stream)))
+
+
+def fem_pattern_export_coo(pat_h, row_offset, I, J, csr_index, stream=None):
+    _check(lib().fem_pattern_export_coo(pat_h, int(row_offset), _ptr(I), _ptr(J), _ptr(csr_index), _stream(stream)))
+
+
+def fem_gather(n, index, src, dst, stream=None):
+    _check(lib().fem_gather(int(n), _ptr(index), _ptr(src), _ptr(dst), _stream(stream)))
 
 
 def fem_get_status(mesh_h, stream=None):

@@ -58,6 +58,17 @@ class FemSystem:
                                out["colidx_s"])
         return out
 
+    def export_coo(self, row_offset=0, values=True):
+        """NEXT-4: the paper's COO view (B-4) in sparse-ID order: dict(I, J, csr_index[, values])
+        with I, J offset by the workpiece's n^dense (row_offset)."""
+        dev = self.device
+        out = {k: torch.empty(self.nnz, dtype=torch.int64, device=dev) for k in ("I", "J", "csr_index")}
+        fem.fem_pattern_export_coo(self.pat_h, row_offset, out["I"], out["J"], out["csr_index"])
+        if values and self.values is not None:
+            out["values"] = torch.empty(self.nnz, dtype=torch.float64, device=dev)
+            fem.fem_gather(self.nnz, out["csr_index"], self.values, out["values"])
+        return out
+
     def matrix(self, state, scatter="atomic", accumulate=False):
         self.alloc(True, False)
         fem.fem_assemble_matrix(self.mesh_h, self.pat_h, self.problem, state, self.values, int(accumulate),

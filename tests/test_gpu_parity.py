@@ -314,3 +314,46 @@ def test_linearize_host_sync_and_pipelined_agree():
     ora = oracle.assemble(m, p, st)
     assert csr_row_scaled_err(ora["rowptr"], S.values.cpu().numpy(), ora["values"]) <= TOL
     S.close()
+
+
+@pytest.mark.parametrize("name,dims", [("c1", (5,)), ("c3", (3, 2, 1)), ("c4", (3, 2, 2)), ("c5", (3, 2, 2))])
+def test_coo_export_matches_oracle_view(name, dims):
+    """NEXT-4: the paper's COO (sparse-ID order, reading L4) exported on the GPU equals the
+    oracle's coo_view bit-exactly (I, J), and the gathered values are the CSR values."""
+    _need_gpu()
+    m, p = make_config(name, "perturbed", dims)
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    ref = oracle.coo_view(ora, m.n_nodes, p.kappa_hat(m.dim), row_offset=7)
+    S = _gpu_system(m, p)
+    S.system(_to_dev(st), scatter="coloured")
+    coo = S.export_coo(row_offset=7)
+    assert np.array_equal(coo["I"].cpu().numpy(), ref["I"]) and np.array_equal(coo["J"].cpu().numpy(), ref["J"])
+    assert np.array_equal(coo["values"].cpu().numpy(), S.values.cpu().numpy()[coo["csr_index"].cpu().numpy()])
+    rp = ora["rowptr"]
+    scale = np.repeat(np.maximum.reduceat(np.abs(ora["values"]), rp[:-1]), np.diff(rp))
+    err = np.abs(coo["values"].cpu().numpy() - ref["values"]) / scale[coo["csr_index"].cpu().numpy()]
+    assert err.max() <= TOL
+    S.close()
+
+
+def test_two_workpieces_block_diagonal_coo():
+    """Two workpieces: their COO blocks at offsets n^dense (rows) and n^sp (sparse IDs) form
+    the block-diagonal system; rows of workpiece 1 never couple to workpiece 0."""
+    _need_gpu()
+    parts = []
+    off_rows = off_sp = 0
+    for name, dims in [("c1", (4,)), ("c5", (2, 2, 2))]:
+        m, p = make_config(name, "perturbed", dims)
+        st = make_state(name, m, p)
+        S = _gpu_system(m, p)
+        S.system(_to_dev(st), scatter="tiled")
+        coo = S.export_coo(row_offset=off_rows)
+        ref = oracle.coo_view(oracle.assemble(m, p, st), m.n_nodes, p.kappa_hat(m.dim), row_offset=off_rows)
+        assert np.array_equal(coo["I"].cpu().numpy(), ref["I"])
+        parts.append((off_sp, coo["I"].cpu().numpy(), coo["J"].cpu().numpy()))
+        off_rows += S.n_rows
+        off_sp += S.nnz
+        S.close()
+    (s0, I0, J0), (s1, I1, J1) = parts
+    assert s1 == len(I0) and I1.min() >= I0.max() + 1 and J1.min() >= J0.max() + 1

@@ -499,3 +499,23 @@ def test_cantilever_deflection_timoshenko():
     tip = np.isclose(m.coords[0], 10.0)
     P, L, E, G, A, I, kappa = 1e-3, 10.0, 1.0, 0.5, 1.0, 1.0 / 12.0, 5.0 / 6.0
     assert abs(-uy[tip].mean() / (P * L ** 3 / (3 * E * I) + P * L / (kappa * G * A)) - 1.0) <= 5e-3
+
+
+@pytest.mark.parametrize("name,dims", [("c1", (4,)), ("c3", (2, 1, 1)), ("c4", (2, 2, 1))])
+def test_coo_view_is_the_csr_in_sparse_id_order(name, dims):
+    """NEXT-4 pin of the COO view (reading L4): a bijection onto the CSR's entries, ordered
+    lexicographically by (κ₀, κ_λ, α₁, α₂), carrying the CSR values; workpiece offsets shift I and J."""
+    m, p = make_config(name, "perturbed", dims)
+    st = make_state(name, m, p)
+    out = oracle.assemble(m, p, st)
+    kh, N = p.kappa_hat(m.dim), m.n_nodes
+    coo = oracle.coo_view(out, N, kh)
+    rp, ci = out["rowptr"], out["colidx"]
+    csr = {(int(r), int(c)): out["values"][k] for r in range(len(rp) - 1) for k, c in zip(range(rp[r], rp[r + 1]), ci[rp[r]:rp[r + 1]])}
+    pairs = list(zip(coo["I"].tolist(), coo["J"].tolist()))
+    assert len(pairs) == len(csr) == len(set(pairs)) and set(pairs) == set(csr)
+    key = [(i // N, j // N, i % N, j % N) for i, j in pairs]
+    assert key == sorted(key)
+    assert all(csr[pq] == v for pq, v in zip(pairs, coo["values"]))
+    off = oracle.coo_view(out, N, kh, row_offset=1000)
+    assert np.array_equal(off["I"], coo["I"] + 1000) and np.array_equal(off["J"], coo["J"] + 1000)
