@@ -44,6 +44,10 @@ def _peaks():
 
 
 FP64_PEAK_TFLOPS = 33.0  # measured DFMA peak on this pool's B200 (profiles/r01_m0_microbench.txt)
+# Algorithmic fp64 flops per element of one matrix+residual step, counted once per element:
+# c5 Q1 hex elasticity, 8 points: J (8·9·8·2 = 1152) + det/J^-1 (8·60 = 480) + G = J^-T ∇̂N (8·8·9·2 = 1152)
+# + Gram M^jk_ab (9·64·8·2 = 9216) + K entries (576·4 = 2304) + r = K'd (576·2 = 1152) = 15456.
+FLOPS_PER_ELEM = {"c5": 15456}
 DMMA_PEAK_TFLOPS = 36.0  # measured fp64 DMMA m8n8k4 peak (profiles/r01_m0b_dmma_smem.txt)
 
 # the record-driven kernel the tiled path launches per configuration (csrc/tiled.cu launch_tiled)
@@ -298,7 +302,12 @@ def main():
                          "kernel": (TILED_KERNEL[name] if args.scatter == "tiled" else f"{args.scatter} kernels")
                          + " (fem_assemble_system)"},
             "fp64": {"peak_tflops": FP64_PEAK_TFLOPS, "peak_kind": "measured DFMA (tools/m0)",
-                     "dmma_peak_tflops": DMMA_PEAK_TFLOPS},
+                     "dmma_peak_tflops": DMMA_PEAK_TFLOPS,
+                     "algorithmic_flops_per_element": FLOPS_PER_ELEM.get(name),
+                     "achieved_tflops": (FLOPS_PER_ELEM[name] * E_total / (ms * 1e-3) / 1e12
+                                         if name in FLOPS_PER_ELEM else None),
+                     "frac": (FLOPS_PER_ELEM[name] * E_total / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS
+                              if name in FLOPS_PER_ELEM else None)},
             "cpu_baseline": cpu,
             "e2e": {"value": E_total / (e2e_ms * 1e-3), "unit": "elements/s",
                     "h2d_bytes_per_step": int(state.nbytes), "d2h_bytes_per_step": 16,
