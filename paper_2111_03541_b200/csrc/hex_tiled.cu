@@ -22,6 +22,16 @@
 
 namespace fem {
 
+// acquire / release on a shared-memory turn counter (scope CTA)
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1])
@@ -525,10 +535,9 @@ __device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t*
   const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
   const RecLayout L = rec_layout_hdr(8, hdr);
   const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
-  for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
-    const int c = t / H, i = t % H, node = hn[i];
-    const double* src = c < 3 ? P.coords + (int64_t)c * P.N + node : P.state + (int64_t)(c - 3) * P.N + node;
-    cp_async8(hbuf + t, src);
+  for (int c = 0; c < P.hcomp; c++) {  // component-major: no integer division per element
+    const double* base = c < 3 ? P.coords + (int64_t)c * P.N : P.state + (int64_t)(c - 3) * P.N;
+    for (int i = threadIdx.x; i < H; i += blockDim.x) cp_async8(hbuf + c * H + i, base + hn[i]);
   }
   cp_async_commit();
 }
@@ -860,10 +869,9 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   if constexpr (ORDERED) {  // wait for this visit's turn on the owned row it writes (record order)
     if (li >= 0) {
       my_turn = (sm + to.vseq)[v * 8 + a];
-      while (*reinterpret_cast<volatile int*>(turn + li) != my_turn)
+      while (ld_acquire_cta(turn + li) != my_turn)  // acquire: the previous holder's row writes are visible
         if (P.spin_ns) __nanosleep(P.spin_ns);
     }
-    __threadfence_block();
   }
   auto write_res = [&]() {  // GEMM residual: lane (a, c < 2) holds r_(a, 2c), r_(a, 2c + 1)
     if (has_rhs && !fuse && c < 2 && li >= 0) {
@@ -913,9 +921,9 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     }
   }
   __syncwarp();  // scratch is reused by the next visit; the row's four lanes have written
-  if constexpr (ORDERED) {  // hand the row to the next visit in record order
-    __threadfence_block();
-    if (c == 0 && li >= 0) *reinterpret_cast<volatile int*>(turn + li) = my_turn + 1;
+  if constexpr (ORDERED) {  // hand the row to the next visit in record order: a release store, cumulative
+    // over the row's four lanes whose writes this lane has observed through __syncwarp
+    if (c == 0 && li >= 0) st_release_cta(turn + li, my_turn + 1);
   }
 }
 
