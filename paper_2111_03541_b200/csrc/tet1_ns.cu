@@ -284,10 +284,9 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_ns_rec(const __grid_consta
       const RecLayout L = rec_layout_hdr(NL, hdr);
       const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
       const int H = hdr[1];
-      for (int t = tid; t < H * P.hcomp; t += blockDim.x) {
-        const int cc = t / H, i = t % H, node = hn[i];
-        const double* src = cc < DIM ? P.coords + (int64_t)cc * P.N + node : P.state + (int64_t)(cc - DIM) * P.N + node;
-        cp_async8(hbuf + t, src);
+      for (int cc = 0; cc < P.hcomp; cc++) {  // component-major: no integer division per element
+        const double* base = cc < DIM ? P.coords + (int64_t)cc * P.N : P.state + (int64_t)(cc - DIM) * P.N;
+        for (int i = tid; i < H; i += blockDim.x) cp_async8(hbuf + cc * H + i, base + hn[i]);
       }
       cp_async_commit();
     }

@@ -239,10 +239,9 @@ __device__ __forceinline__ void p2_gather_halo(const TiledParams& P, const uint8
   const RecLayout L = rec_layout_hdr(10, hdr);
   const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
   const int H = hdr[1];
-  for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
-    const int cc = t / H, i = t % H, node = hn[i];
-    const double* src = cc < 3 ? P.coords + (int64_t)cc * P.N + node : P.state + (int64_t)(cc - 3) * P.N + node;
-    cp_async8(hbuf + t, src);
+  for (int cc = 0; cc < P.hcomp; cc++) {  // component-major: no integer division per element
+    const double* base = cc < 3 ? P.coords + (int64_t)cc * P.N : P.state + (int64_t)(cc - 3) * P.N;
+    for (int i = threadIdx.x; i < H; i += blockDim.x) cp_async8(hbuf + cc * H + i, base + hn[i]);
   }
   cp_async_commit();
 }
