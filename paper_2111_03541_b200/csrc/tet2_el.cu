@@ -41,6 +41,8 @@ struct P2Coef {
   double cl, cm, sl, sm;  // Σ f0 λ, Σ f0 μ (matrix); Σ λ, Σ μ (residual)
 };
 
+// HAS_V / HAS_R: the call kind (matrix, residual, both) fixed per launch, so each body compiles lean
+template <bool HAS_V, bool HAS_R>
 __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to, const P2Coef& H,
                                          const double* __restrict__ lt, double* sc, int v, unsigned char* sm) {
   const int lane = threadIdx.x & 31;
@@ -49,7 +51,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
   const uint16_t* hv = reinterpret_cast<const uint16_t*>(sm + to.vhal) + v * 10;
   const double* hdat = reinterpret_cast<const double*>(sm + to.hdat);
   const int HH = to.H;
-  const double* L = lt + lane * P2_LANE_TAB;
+  const double* L = lt + lane;  // lane table, transposed: L[32 k] = constant k of this lane (conflict-free)
   // ---- geometry GEMM
   double C2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
@@ -57,7 +59,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
     const int k = 4 * s + c;
     const double av = (r < 6 && k < 10) ? hdat[r * HH + hv[k]] : 0.0;
 #pragma unroll
-    for (int t = 0; t < 2; t++) dmma884_t2(C2[t], av, L[s * 2 + t]);
+    for (int t = 0; t < 2; t++) dmma884_t2(C2[t], av, L[32 * (s * 2 + t)]);
   }
   if (r < 6) {
 #pragma unroll
@@ -77,7 +79,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
 #pragma unroll
     for (int j = 0; j < 3; j++) {
       J[i][j] = sc[i * 12 + 3 * q + j];
-      Dr[i][j] = sc[(3 + i) * 12 + 3 * q + j];
+      if constexpr (HAS_R) Dr[i][j] = sc[(3 + i) * 12 + 3 * q + j];
     }
   const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
   const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
@@ -101,11 +103,6 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
     Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
     Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
     Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
-    double gu[3][3];
-#pragma unroll
-    for (int k = 0; k < 3; k++)
-#pragma unroll
-      for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
     double* o = sc + q * 20;
 #pragma unroll
     for (int j = 0; j < 3; j++)
@@ -113,11 +110,18 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
       for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
     const double w = det * (1.0 / 24.0);  // 4-point rule weight 1/24
     o[9] = w;
-    const double lw = H.sl * w * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * w;
+    if constexpr (HAS_R) {
+      double gu[3][3];
 #pragma unroll
-    for (int i = 0; i < 3; i++)
+      for (int k = 0; k < 3; k++)
 #pragma unroll
-      for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+        for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+      const double lw = H.sl * w * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * w;
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+    }
   }
   __syncwarp();
   // ---- fragment layout: lane (a0, c) holds G of node a0 and of node a1 = 8 + (a0 & 1) at point c
@@ -126,12 +130,12 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
   double G0[3], G1[3];
 #pragma unroll
   for (int i = 0; i < 3; i++) {
-    G0[i] = o[0 * 3 + i] * L[6] + o[1 * 3 + i] * L[7] + o[2 * 3 + i] * L[8];
-    G1[i] = o[0 * 3 + i] * L[9] + o[1 * 3 + i] * L[10] + o[2 * 3 + i] * L[11];
+    G0[i] = o[0 * 3 + i] * L[32 * 6] + o[1 * 3 + i] * L[32 * 7] + o[2 * 3 + i] * L[32 * 8];
+    G1[i] = o[0 * 3 + i] * L[32 * 9] + o[1 * 3 + i] * L[32 * 10] + o[2 * 3 + i] * L[32 * 11];
   }
   const double w = o[9];
   const int li0 = own[a0], li1 = own[a1];
-  if (P.rhs) {  // r_(a,i) = -Σ_γ w σ_ij G_aj, reduced over the 4 points (lanes c)
+  if constexpr (HAS_R) {  // r_(a,i) = -Σ_γ w σ_ij G_aj, reduced over the 4 points (lanes c)
 #pragma unroll
     for (int i = 0; i < 3; i++) {
       double t0 = 0.0, t1 = 0.0;
@@ -147,7 +151,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
       if (c == 0 && r < 2 && li1 >= 0) atomicAdd(racc + i * to.T + li1, t1);
     }
   }
-  if (!P.values) {
+  if constexpr (!HAS_V) {
     __syncwarp();
     return;
   }
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) {  // per-lane constants: GEMM B fragments and reference gradients at the lane's point
     using EL = Elem<ET_TET, 2>;
-    double* Lt = lanetab + tid * P2_LANE_TAB;
+    double* Lt = lanetab + tid;  // transposed: constant k of lane l at 32 k + l
     for (int s = 0; s < 3; s++)
       for (int t = 0; t < 2; t++) {
         const int k = 4 * s + (tid & 3), n = 8 * t + (tid >> 2);
@@ -285,15 +289,15 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
           EL::shape(xi, N, dN);
           val = dN[k][n % 3];
         }
-        Lt[s * 2 + t] = val;
+        Lt[32 * (s * 2 + t)] = val;
       }
     double xi[3], wq, N[10], dN[10][3];
     EL::vol_qp(2, tid & 3, xi, wq);
     EL::shape(xi, N, dN);
     const int a0 = tid >> 2, a1 = 8 + (a0 & 1);
     for (int i = 0; i < 3; i++) {
-      Lt[6 + i] = dN[a0][i];
-      Lt[9 + i] = dN[a1][i];
+      Lt[32 * (6 + i)] = dN[a0][i];
+      Lt[32 * (9 + i)] = dN[a1][i];
     }
   }
   int64_t tile = blockIdx.x;
@@ -339,7 +343,12 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
     cp_async_wait_all();
     __syncthreads();
     double* wsc = reinterpret_cast<double*>(F.qp) + (size_t)P2_SCRATCH * warp;
-    for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit(P, to, Hc, lanetab, wsc, v, smem);
+    if (P.values && P.rhs)
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<true, true>(P, to, Hc, lanetab, wsc, v, smem);
+    else if (P.values)
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<true, false>(P, to, Hc, lanetab, wsc, v, smem);
+    else
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<false, true>(P, to, Hc, lanetab, wsc, v, smem);
     if (next < P.n_tiles) {
       mbar_wait(&mbar[oth], (uint32_t)(((it + 1) >> 1) & 1));
       p2_gather_halo(P, P2RBUF(oth), P2HBUF(oth));
