@@ -186,6 +186,28 @@ int fem_pattern_export_coo(fem_pattern_t pat, int64_t row_offset, int64_t* I, in
                            void* stream);
 int fem_gather(int64_t n, const int64_t* index, const double* src, double* dst, void* stream);
 
+/* ---- NEXT-3: generalized-α time stepping around the assembly (Block C P:404-417, D-1 P:421-424,
+ * D-4 P:459-465; Eqs. time_constraints/time_effective P:226-236).  All arrays DEVICE float64, layout
+ * [ν][n] (ν = 0..ts->nu_hat, n = rows of the system = κ̂N, κ-major), caller-owned, stream-ordered, no
+ * host sync.  phi0 = committed values ∂_t^ν φ, incr = increments Δ∂_t^ν φ, eff = effective values
+ * ∂_t^ν φ̃ (the `state` input of the assembly calls).  Values are the correctly rounded left-to-right
+ * evaluation of the expressions below (no FMA contraction).  Errors: INVALID_ARG (ts NULL, kind not
+ * FEM_TIME_GENALPHA, nu_hat outside 0..2, dt <= 0, b_ν = 0 for a ν <= nu_hat that divides, n < 0,
+ * NULL arrays), CUDA.
+ *
+ * fem_time_init — Block C.  C-1: phi0[ν] += incr[ν]; C-2: incr[ν̂] = 0; C-3 (reading L14, Eq.
+ *   time_constraints): incr[ν] = dt·(phi0[ν+1] + b_{ν+1}·incr[ν+1]) for ν = ν̂-1 … 0.  If eff != NULL
+ *   also writes D-1 of the first sub-step (fused, same pass).
+ * fem_time_effective — D-1: eff[ν] = c_{ν+1}·incr[ν] + phi0[ν].
+ * fem_time_increment — D-4 (reading L13): incr[ν] += delta_sub / Π_{β'=1}^{ν}(b_β'·dt), delta_sub [n]
+ *   the solve's sub-step increment Δ_sub φ; if eff != NULL (then phi0 is required) also writes D-1 of the
+ *   next sub-step in the same pass. */
+int fem_time_init(const fem_time_scheme* ts, int64_t n, double* phi0, double* incr, double* eff, void* stream);
+int fem_time_effective(const fem_time_scheme* ts, int64_t n, const double* phi0, const double* incr, double* eff,
+                       void* stream);
+int fem_time_increment(const fem_time_scheme* ts, int64_t n, const double* delta_sub, double* incr,
+                       const double* phi0, double* eff, void* stream);
+
 /* fem_get_status — synchronizes `stream`; returns 0 or FEM_E_INVERTED_ELEMENT (bad_elem = an
  * offending element id, else -1).  Resets the device error word. */
 int fem_get_status(fem_mesh_t mesh, void* stream, int64_t* bad_elem);

@@ -139,6 +139,10 @@ def lib():
         L.fem_bicgstab_work_doubles.restype = I64
         L.fem_bicgstab_solve.argtypes = [I64, V, V, V, V, V, I, C.c_double, I, V, C.POINTER(I),
                                          C.POINTER(C.c_double), V]
+        PT = C.POINTER(fem_time_scheme)
+        L.fem_time_init.argtypes = [PT, I64, V, V, V, V]
+        L.fem_time_effective.argtypes = [PT, I64, V, V, V, V]
+        L.fem_time_increment.argtypes = [PT, I64, V, V, V, V, V]
         L.fem_last_error.restype = C.c_char_p
         L.fem_version.restype = I
         _lib = L
@@ -149,7 +153,8 @@ EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pa
             "fem_assemble_matrix", "fem_assemble_residual", "fem_assemble_system", "fem_residual_norms",
             "fem_linearize_host", "fem_linearize_host_async", "fem_pattern_export_coo", "fem_gather", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
-            "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve"]
+            "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve",
+            "fem_time_init", "fem_time_effective", "fem_time_increment"]
 
 
 def _check(rc):
@@ -310,6 +315,28 @@ def fem_pattern_export_coo(pat_h, row_offset, I, J, csr_index, stream=None):
 
 def fem_gather(n, index, src, dst, stream=None):
     _check(lib().fem_gather(int(n), _ptr(index), _ptr(src), _ptr(dst), _stream(stream)))
+
+
+def make_time_scheme(t) -> fem_time_scheme:
+    """Marshal a TimeScheme (kind/nu_hat/dt/b1/b2/c1/c2/c3) for the NEXT-3 time-stepping calls."""
+    T = fem_time_scheme()
+    T.kind = 1 if t.kind == "genalpha" else 0
+    T.nu_hat = t.nu_hat
+    T.dt, T.b1, T.b2, T.c1, T.c2, T.c3 = t.dt, t.b1, t.b2, t.c1, t.c2, t.c3
+    return T
+
+
+def fem_time_init(ts, n, phi0, incr, eff=None, stream=None):
+    _check(lib().fem_time_init(C.byref(ts), int(n), _ptr(phi0), _ptr(incr), _ptr(eff), _stream(stream)))
+
+
+def fem_time_effective(ts, n, phi0, incr, eff, stream=None):
+    _check(lib().fem_time_effective(C.byref(ts), int(n), _ptr(phi0), _ptr(incr), _ptr(eff), _stream(stream)))
+
+
+def fem_time_increment(ts, n, delta_sub, incr, phi0=None, eff=None, stream=None):
+    _check(lib().fem_time_increment(C.byref(ts), int(n), _ptr(delta_sub), _ptr(incr), _ptr(phi0), _ptr(eff),
+                                    _stream(stream)))
 
 
 def fem_get_status(mesh_h, stream=None):

@@ -131,6 +131,35 @@ class FemSystem:
         new[0] += dx.view(self.kh, self.N)
         return new, it, rel
 
+    # ---- NEXT-3: one generalized-alpha timestep (Blocks C and D) on the GPU
+    def time_step(self, phi0, incr, n_sub=1, scatter="tiled", method="bicgstab", spd_sign=-1.0, rtol=1e-12,
+                  max_iter=20000, tol=0.0):
+        """Advance one timestep with the problem's generalized-alpha scheme, in place on the DEVICE arrays
+        phi0 (committed ∂^ν φ) and incr (Δ∂^ν φ), both float64 [ν̂+1][κ̂][N].  Block C (fem_time_init,
+        fused with the first D-1), then up to n_sub sub-steps: assemble K, d at the effective values (D-2,
+        D-3), solve K Δ_sub = -d (D-4, fem_cg/bicgstab), fem_time_increment (fused with the next D-1);
+        stops early when ||d||_2 <= tol.  Returns the list of (||d||_2 before the solve, iterations)."""
+        t = self.problem.time
+        if t.kind != "genalpha":
+            raise ValueError("time_step needs a genalpha problem")
+        ts = fem.make_time_scheme(t)
+        n = self.kh * self.N
+        eff = getattr(self, "_eff", None)
+        if eff is None or eff.shape != phi0.shape:
+            eff = self._eff = torch.empty_like(phi0)
+        fem.fem_time_init(ts, n, phi0, incr, eff)
+        hist = []
+        for _ in range(n_sub):
+            K, d = self.system(eff, scatter=scatter)
+            dn = float(torch.linalg.vector_norm(d))
+            if dn <= tol:
+                hist.append((dn, 0))
+                break
+            dx, it, _ = self.solve(-d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method)
+            fem.fem_time_increment(ts, n, dx, incr, phi0, eff)
+            hist.append((dn, it))
+        return hist
+
     def norms(self, rhs=None):
         out = torch.empty(2, dtype=torch.float64, device=self.device)
         fem.fem_residual_norms(self.mesh_h, self.rhs if rhs is None else rhs, out)
