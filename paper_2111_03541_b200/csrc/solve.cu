@@ -87,17 +87,66 @@ __device__ __forceinline__ double row_dot(int64_t r, int64_t n, int sub, const i
   return acc;
 }
 
+// G = 0: a warp owns 32 consecutive rows.  Lane i loads rowptr[r0+i] (one coalesced load, no rowptr
+// latency per row), then the warp walks its rows two at a time, each lane issuing up to 6 predicated
+// value/column loads per trip (3 strided chunks per row: a c5 row of 81 entries is one trip) so two
+// rows' loads are in flight together.  Per-lane sums and the xor tree are the G = 32 order, so
+// results are bit-identical to row_dot<32>.  Lane i returns row r0+i's dot.
+__device__ __forceinline__ double rows32_dot(int64_t r0, int64_t n, int lane, const int64_t* __restrict__ rowptr,
+                                             const int32_t* __restrict__ colidx, const double* __restrict__ val,
+                                             const double* __restrict__ x) {
+  const int64_t b = rowptr[r0 + lane < n ? r0 + lane : n], e = rowptr[r0 + lane + 1 < n ? r0 + lane + 1 : n];
+  double mine = 0.0;
+  for (int i = 0; i < 32; i += 2) {
+    const int64_t s0 = __shfl_sync(0xffffffffu, b, i), l0 = __shfl_sync(0xffffffffu, e, i) - s0;
+    const int64_t s1 = __shfl_sync(0xffffffffu, b, i + 1), l1 = __shfl_sync(0xffffffffu, e, i + 1) - s1;
+    const int64_t len = l0 > l1 ? l0 : l1;
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t off = lane; off < len; off += 96) {
+      double v[6];
+      int32_t c[6];
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        const int64_t o = off + 32 * j;
+        v[j] = o < l0 ? __ldcs(val + s0 + o) : 0.0;
+        c[j] = o < l0 ? __ldcs(colidx + s0 + o) : -1;
+        v[3 + j] = o < l1 ? __ldcs(val + s1 + o) : 0.0;
+        c[3 + j] = o < l1 ? __ldcs(colidx + s1 + o) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        if (c[j] >= 0) a0 = fma(v[j], __ldg(x + c[j]), a0);
+        if (c[3 + j] >= 0) a1 = fma(v[3 + j], __ldg(x + c[3 + j]), a1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (lane == i) mine = a0;
+    if (lane == i + 1) mine = a1;
+  }
+  return mine;
+}
+template <int G>
+__device__ __forceinline__ double rows_dot(int64_t r0, int64_t r, int64_t n, int sub, int lane,
+                                           const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+                                           const double* __restrict__ val, const double* __restrict__ x) {
+  if constexpr (G == 0) return rows32_dot(r0, n, lane, rowptr, colidx, val, x);
+  else return row_dot<G>(r, n, sub, rowptr, colidx, val, x);
+}
 template <int G>
 __global__ void __launch_bounds__(SV_THREADS) k_spmv(int64_t n, const int64_t* __restrict__ rowptr,
                                                      const int32_t* __restrict__ colidx,
                                                      const double* __restrict__ val, const double* __restrict__ x,
                                                      double* __restrict__ y, double alpha, double beta) {
-  constexpr int RPW = 32 / G;  // rows per warp and step
-  const int lane = threadIdx.x & 31, sub = lane % G;
+  constexpr int RPW = G ? 32 / (G ? G : 1) : 32;  // rows per warp and step
+  const int lane = threadIdx.x & 31, sub = G ? lane % (G ? G : 1) : 0;
   const int64_t nwarps = (int64_t)gridDim.x * (SV_THREADS / 32);
   for (int64_t w = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) / 32; w * RPW < n; w += nwarps) {
-    const int64_t r = w * RPW + lane / G;
-    const double acc = row_dot<G>(r, n, sub, rowptr, colidx, val, x);
+    const int64_t r = w * RPW + (G ? lane / (G ? G : 1) : lane);
+    const double acc = rows_dot<G>(w * RPW, r, n, sub, lane, rowptr, colidx, val, x);
     if (sub == 0 && r < n) y[r] = alpha * acc + (beta == 0.0 ? 0.0 : beta * y[r]);
   }
 }
@@ -109,13 +158,13 @@ __global__ void __launch_bounds__(SV_THREADS) k_cg_spmv(int64_t n, const int64_t
                                                         const double* __restrict__ val, double s,
                                                         const double* __restrict__ p, double* __restrict__ q,
                                                         double* partials, CgScal* sc) {
-  constexpr int RPW = 32 / G;
-  const int lane = threadIdx.x & 31, sub = lane % G;
+  constexpr int RPW = G ? 32 / (G ? G : 1) : 32;
+  const int lane = threadIdx.x & 31, sub = G ? lane % (G ? G : 1) : 0;
   const int64_t nwarps = (int64_t)gridDim.x * (SV_THREADS / 32);
   double dot = 0.0;
   for (int64_t w = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) / 32; w * RPW < n; w += nwarps) {
-    const int64_t r = w * RPW + lane / G;
-    const double acc = row_dot<G>(r, n, sub, rowptr, colidx, val, p);
+    const int64_t r = w * RPW + (G ? lane / (G ? G : 1) : lane);
+    const double acc = rows_dot<G>(w * RPW, r, n, sub, lane, rowptr, colidx, val, p);
     if (sub == 0 && r < n) {
       const double qr = s * acc;
       q[r] = qr;
@@ -359,13 +408,13 @@ __global__ void __launch_bounds__(SV_THREADS) k_bi_spmv(int64_t n, const int64_t
                                                         const double* __restrict__ val, const double* __restrict__ in,
                                                         double* __restrict__ out, const double* __restrict__ a,
                                                         double* partials, BiScal* sc) {
-  constexpr int RPW = 32 / G;
-  const int lane = threadIdx.x & 31, sub = lane % G;
+  constexpr int RPW = G ? 32 / (G ? G : 1) : 32;
+  const int lane = threadIdx.x & 31, sub = G ? lane % (G ? G : 1) : 0;
   const int64_t nwarps = (int64_t)gridDim.x * (SV_THREADS / 32);
   double d0 = 0.0, d1 = 0.0;
   for (int64_t w = ((int64_t)blockIdx.x * SV_THREADS + threadIdx.x) / 32; w * RPW < n; w += nwarps) {
-    const int64_t r = w * RPW + lane / G;
-    const double acc = row_dot<G>(r, n, sub, rowptr, colidx, val, in);
+    const int64_t r = w * RPW + (G ? lane / (G ? G : 1) : lane);
+    const double acc = rows_dot<G>(w * RPW, r, n, sub, lane, rowptr, colidx, val, in);
     if (sub == 0 && r < n) {
       out[r] = acc;
       d0 = fma(a[r], acc, d0);
@@ -461,8 +510,8 @@ __global__ void __launch_bounds__(SV_THREADS) k_bi_init(int64_t n, const int64_t
 // lanes per CSR row of the SpMV kernels (FEM_SPMV_LANES = 8 | 16 | 32 for A/B runs)
 static int spmv_lanes() {
   const char* e = getenv("FEM_SPMV_LANES");
-  const int g = e ? atoi(e) : 32;  // c5: 32 lanes 12.8 ms, 16 lanes 13.8 ms, 8 lanes 14.6 ms per SpMV
-  return (g == 16 || g == 32) ? g : 8;
+  const int g = e ? atoi(e) : 0;  // c5: warp-owned 32-row blocks 11.4 ms; 32 lanes/row 12.8, 16: 13.8, 8: 14.6 ms
+  return (g == 0 || g == 16 || g == 32) ? g : 8;
 }
 
 static int grid_for(int64_t n, int per_thread_rows) {
@@ -494,7 +543,8 @@ extern "C" int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* co
     return 0;
   }
   const int g = spmv_lanes();
-  if (g == 32) k_spmv<32><<<grid_for(n_rows, 32), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  if (g == 0) k_spmv<0><<<grid_for(n_rows, 1), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  else if (g == 32) k_spmv<32><<<grid_for(n_rows, 32), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
   else if (g == 16) k_spmv<16><<<grid_for(n_rows, 16), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
   else k_spmv<8><<<grid_for(n_rows, 8), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
   FEM_CUDA_TRY(cudaGetLastError());
@@ -525,7 +575,7 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
   int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(CgScal));
   FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(CgScal) + 8, s));
   const int g = spmv_lanes();
-  const int gv = grid_for(n, 1), gm = grid_for(n, g);
+  const int gv = grid_for(n, 1), gm = grid_for(n, g ? g : 1);
   const bool tma = getenv("FEM_SPMV_TMA") != nullptr;
   const int gt = (int)std::min<int64_t>((n + SP_ROWS - 1) / SP_ROWS, 2 * 148);
   if (tma) FEM_CUDA_TRY(cudaFuncSetAttribute(k_spmv_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spmv_tma_smem()));
@@ -549,6 +599,7 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
     const int todo = std::min(chk, max_iter - it);
     for (int k = 0; k < todo; k++) {
       if (tma) k_spmv_tma<1><<<gt, SP_THREADS, spmv_tma_smem(), s>>>(n, rowptr, colidx, values, p, q, spd_sign, 0.0, partials, sc);
+      else if (g == 0) k_cg_spmv<0><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
       else if (g == 32) k_cg_spmv<32><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
       else if (g == 16) k_cg_spmv<16><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
       else k_cg_spmv<8><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
@@ -593,7 +644,7 @@ extern "C" int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const i
   int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(BiScal));
   FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(BiScal) + 8, st));
   const int g = spmv_lanes();
-  const int gv = grid_for(n, 1), gm = grid_for(n, g);
+  const int gv = grid_for(n, 1), gm = grid_for(n, g ? g : 1);
   k_bi_init<<<gv, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, b, x, r, rh, dinv, partials, sc, bad);
   FEM_CUDA_TRY(cudaGetLastError());
   BiScal h{};
@@ -614,7 +665,8 @@ extern "C" int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const i
     for (int k = 0; k < todo; k++) {
       k_bi_dir<<<gv, SV_THREADS, 0, st>>>(n, r, p, v, dinv, y, sc, it + k == 0);
 #define BI_SPMV(MODE, IN, OUT, A)                                                                                 \
-  if (g == 32) k_bi_spmv<32, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
+  if (g == 0) k_bi_spmv<0, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
+  else if (g == 32) k_bi_spmv<32, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
   else if (g == 16) k_bi_spmv<16, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
   else k_bi_spmv<8, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc);
       BI_SPMV(0, y, v, rh)
