@@ -92,48 +92,57 @@ __device__ __forceinline__ double row_dot(int64_t r, int64_t n, int sub, const i
 // value/column loads per trip (3 strided chunks per row: a c5 row of 81 entries is one trip) so two
 // rows' loads are in flight together.  Per-lane sums and the xor tree are the G = 32 order, so
 // results are bit-identical to row_dot<32>.  Lane i returns row r0+i's dot.
+template <int R>
 __device__ __forceinline__ double rows32_dot(int64_t r0, int64_t n, int lane, const int64_t* __restrict__ rowptr,
                                              const int32_t* __restrict__ colidx, const double* __restrict__ val,
                                              const double* __restrict__ x) {
   const int64_t b = rowptr[r0 + lane < n ? r0 + lane : n], e = rowptr[r0 + lane + 1 < n ? r0 + lane + 1 : n];
   double mine = 0.0;
-  for (int i = 0; i < 32; i += 2) {
-    const int64_t s0 = __shfl_sync(0xffffffffu, b, i), l0 = __shfl_sync(0xffffffffu, e, i) - s0;
-    const int64_t s1 = __shfl_sync(0xffffffffu, b, i + 1), l1 = __shfl_sync(0xffffffffu, e, i + 1) - s1;
-    const int64_t len = l0 > l1 ? l0 : l1;
-    double a0 = 0.0, a1 = 0.0;
+  for (int i = 0; i < 32; i += R) {
+    int64_t s0[R], l0[R], len = 0;
+    double a[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      s0[q] = __shfl_sync(0xffffffffu, b, i + q);
+      l0[q] = __shfl_sync(0xffffffffu, e, i + q) - s0[q];
+      len = l0[q] > len ? l0[q] : len;
+      a[q] = 0.0;
+    }
     for (int64_t off = lane; off < len; off += 96) {
-      double v[6];
-      int32_t c[6];
+      double v[3 * R];
+      int32_t c[3 * R];
 #pragma unroll
-      for (int j = 0; j < 3; j++) {
-        const int64_t o = off + 32 * j;
-        v[j] = o < l0 ? __ldcs(val + s0 + o) : 0.0;
-        c[j] = o < l0 ? __ldcs(colidx + s0 + o) : -1;
-        v[3 + j] = o < l1 ? __ldcs(val + s1 + o) : 0.0;
-        c[3 + j] = o < l1 ? __ldcs(colidx + s1 + o) : -1;
-      }
+      for (int q = 0; q < R; q++)
 #pragma unroll
-      for (int j = 0; j < 3; j++) {
-        if (c[j] >= 0) a0 = fma(v[j], __ldg(x + c[j]), a0);
-        if (c[3 + j] >= 0) a1 = fma(v[3 + j], __ldg(x + c[3 + j]), a1);
-      }
+        for (int j = 0; j < 3; j++) {
+          const int64_t o = off + 32 * j;
+          v[3 * q + j] = o < l0[q] ? __ldcs(val + s0[q] + o) : 0.0;
+          c[3 * q + j] = o < l0[q] ? __ldcs(colidx + s0[q] + o) : -1;
+        }
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int q = 0; q < R; q++)
+          if (c[3 * q + j] >= 0) a[q] = fma(v[3 * q + j], __ldg(x + c[3 * q + j]), a[q]);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-    }
-    if (lane == i) mine = a0;
-    if (lane == i + 1) mine = a1;
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < R; q++) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+#pragma unroll
+    for (int q = 0; q < R; q++)
+      if (lane == i + q) mine = a[q];
   }
   return mine;
 }
+#ifndef FEM_SPMV_R
+#define FEM_SPMV_R 2
+#endif
 template <int G>
 __device__ __forceinline__ double rows_dot(int64_t r0, int64_t r, int64_t n, int sub, int lane,
                                            const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
                                            const double* __restrict__ val, const double* __restrict__ x) {
-  if constexpr (G == 0) return rows32_dot(r0, n, lane, rowptr, colidx, val, x);
+  if constexpr (G == 0) return rows32_dot<FEM_SPMV_R>(r0, n, lane, rowptr, colidx, val, x);
   else return row_dot<G>(r, n, sub, rowptr, colidx, val, x);
 }
 template <int G>
