@@ -32,7 +32,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-sum of v, then the last block to arrive sums the per-block partials in block order.
+// Block-sum of v, then the last block to arrive sums the per-block partials in a fixed order.
 // Returns true in thread 0 of that last block, with *out written.
 template <int NT = SV_THREADS>
 __device__ __forceinline__ bool block_reduce_last(double v, double* partials, unsigned int* ticket, double* out) {
@@ -51,10 +51,18 @@ __device__ __forceinline__ bool block_reduce_last(double v, double* partials, un
   __syncthreads();
   if (!last) return false;
   __threadfence();
+  // the whole last block sums the partials: thread j takes blocks j, j+NT, … in order, then the fixed
+  // xor tree and the warp totals in warp order — a fixed order (bit-reproducible) without a 1000-long
+  // serial chain of L2 loads in one thread
+  double t = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += NT) t += __ldcg(partials + i);
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;  // thread 0 finished reading ws before the barrier
+  __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (unsigned i = 0; i < gridDim.x; i++) t += reinterpret_cast<volatile double*>(partials)[i];
-    *out = t;
+    double b = 0.0;
+    for (int i = 0; i < NT / 32; i++) b += ws[i];
+    *out = b;
     *ticket = 0u;
   }
   return threadIdx.x == 0;
