@@ -531,6 +531,22 @@ static int spmv_lanes() {
   return (g == 0 || g == 16 || g == 32) ? g : 8;
 }
 
+// Row mapping for the solvers' SpMVs from the average row length (one 8-byte read + sync at solve start,
+// next to the init sync the solvers already do): long rows (Q1 elasticity, 81) take the warp-owned
+// 32-row blocks, short rows (scalar Q1, 27) 8 lanes per row (c2 transient: 8 lanes beat the row blocks
+// by 7%).  FEM_SPMV_LANES overrides.
+static int solver_lanes(const int64_t* rowptr, int64_t n, cudaStream_t s, int* g) {
+  if (getenv("FEM_SPMV_LANES")) {
+    *g = spmv_lanes();
+    return 0;
+  }
+  int64_t nnz = 0;
+  FEM_CUDA_TRY(cudaMemcpyAsync(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA_TRY(cudaStreamSynchronize(s));
+  *g = (n > 0 && nnz >= 48 * n) ? 0 : 8;
+  return 0;
+}
+
 static int grid_for(int64_t n, int per_thread_rows) {
   const int64_t need = (n * per_thread_rows + SV_THREADS - 1) / SV_THREADS;
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, SV_MAX_BLOCKS));
@@ -591,7 +607,8 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
   CgScal* sc = reinterpret_cast<CgScal*>(partials + 2 * SV_MAX_BLOCKS);
   int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(CgScal));
   FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(CgScal) + 8, s));
-  const int g = spmv_lanes();
+  int g = 0;
+  if (int rc = solver_lanes(rowptr, n, s, &g)) return rc;
   const int gv = grid_for(n, 1), gm = grid_for(n, g ? g : 1);
   const bool tma = getenv("FEM_SPMV_TMA") != nullptr;
   const int gt = (int)std::min<int64_t>((n + SP_ROWS - 1) / SP_ROWS, 2 * 148);
@@ -660,7 +677,8 @@ extern "C" int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const i
   BiScal* sc = reinterpret_cast<BiScal*>(partials + 2 * SV_MAX_BLOCKS);
   int* bad = reinterpret_cast<int*>(reinterpret_cast<char*>(sc) + sizeof(BiScal));
   FEM_CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(BiScal) + 8, st));
-  const int g = spmv_lanes();
+  int g = 0;
+  if (int rc = solver_lanes(rowptr, n, st, &g)) return rc;
   const int gv = grid_for(n, 1), gm = grid_for(n, g ? g : 1);
   k_bi_init<<<gv, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, b, x, r, rh, dinv, partials, sc, bad);
   FEM_CUDA_TRY(cudaGetLastError());
