@@ -105,3 +105,27 @@ def test_linear_problem_converges_in_one_substep():
     r = ot.step_linear(ts, 2, mats, f, phi0, incr, n_sub=1)
     scale = max(np.linalg.norm(m, 2) for m in mats) * np.abs(phi0).max() / ts["dt"] ** 2
     assert r <= 1e-11 * scale
+
+
+def _hf_amplitude_ratio(ts, w=1e4, steps=40):
+    mats = [np.array([[w * w]]), np.zeros((1, 1)), np.array([[1.0]])]
+    phi0 = np.array([[1.0], [0.0], [-w * w]])
+    incr = np.zeros_like(phi0)
+    E = []
+    for _ in range(steps):
+        ot.step_linear(ts, 2, mats, np.zeros(1), phi0, incr)
+        s = ot.committed(2, phi0, incr)
+        E.append(0.5 * s[1, 0] ** 2 + 0.5 * w * w * s[0, 0] ** 2)
+    return (E[-1] / E[0]) ** (1.0 / (2 * (steps - 1)))
+
+
+def test_second_order_members_do_not_damp_high_frequencies():
+    """Reading L26: Eq. time_constraints is a Newmark update exactly when b1 = 1/2, with β = b1·b2 = γ/2,
+    γ = b2; the second-order condition of generalized-α then forces γ = 1/2, β = 1/4 — the
+    non-dissipative member.  SPEC's 'visible damping at ρ∞ = 0' is not reachable in this family:
+    the per-step amplitude at ωΔt = 1e4 is 1 for every ρ∞ knob, while a first-order member
+    (γ = b2 = 0.9) damps."""
+    for rho in (0.0, 0.5, 1.0):
+        assert _hf_amplitude_ratio(dict(dt=1.0, **ot.genalpha_rho(rho))) == pytest.approx(1.0, abs=1e-6)
+    damped = _hf_amplitude_ratio(dict(dt=1.0, b1=0.5, b2=0.9, c1=1.0, c2=1.0, c3=1.0))
+    assert damped < 0.9
