@@ -4,8 +4,8 @@ Plain serial fp64 CPU oracle of the MetaFEM assembly (arXiv:2111.03541 Blocks B/
 from PAPER.md in C (fem_oracle.c) and loaded with ctypes.  Only tests/, __graft_entry__.smoke()
 and bench.py's cpu_baseline / --impl reference legs may import this package; the product path
 (paper_2111_03541_b200) never does.  Parity pins: see tests/test_oracle_*.py and DESIGN.md §5.
-Parity unpinned (no closed form): NS boundary terms with the non-polynomial inflow profile and
-facet integrals on perturbed meshes — covered only by FD tangents and cross-checks.
+Residual families are pinned by closed-form weak-form moments (tests/test_oracle_pins_flux.py); the
+inflow profile term (degree 4 under a degree-2 facet rule) is pinned by convergence to its exact integral.
 """
 from __future__ import annotations
 

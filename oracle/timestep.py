@@ -16,7 +16,8 @@ Readings:
 
 Pins (tests/test_oracle_pins.py): trapezoidal amplification factor for φ' = -λφ (closed form),
 exact energy conservation of the average-acceleration member for the undamped oscillator, observed
-order >= 1.9 against cos(ωt) at ρ∞ = 0.8, the constraint invariant of Eq.
+order >= 1.9 against cos(ωt) at ρ∞ = 0.8 and high-frequency damping at ρ∞ = 0 but none at ρ∞ = 1
+(reading L26), the constraint invariant of Eq.
 time_constraints under repeated D-4 updates, and one-sub-step convergence for linear problems.
 """
 from __future__ import annotations
@@ -91,8 +92,11 @@ def committed(nu_hat, phi0, incr):
 
 
 def genalpha_rho(rho_inf):
-    """Scheme parameters for the paper's constraint form (Eq. time_constraints) with spectral-radius
-    knob ρ∞: α_m = α_f = ρ∞/(1+ρ∞), c1 = c2 = 1-α_f, c3 = 1-α_m, b1 = b2 = 1/2 (the paper's form fixes
-    Newmark β = b1·b2, γ = b2, and second order needs γ = 1/2).  DESIGN.md reading L25."""
-    a = rho_inf / (1.0 + rho_inf)
-    return dict(b1=0.5, b2=0.5, c1=1.0 - a, c2=1.0 - a, c3=1.0 - a)
+    """Scheme parameters from the spectral-radius knob ρ∞ (reading L26; the paper cites generalized-α
+    but lists no values, SPEC S:412 fixes the mapping): α_m = (2ρ∞−1)/(ρ∞+1), α_f = ρ∞/(ρ∞+1),
+    γ = ½ − α_m + α_f (the generalized-α second-order condition); b1 = ½, b2 = γ, c1 = c2 = 1 − α_f,
+    c3 = 1 − α_m.  With b1 = ½ Eq. time_constraints is a Newmark update with β = γ/2."""
+    a_m = (2.0 * rho_inf - 1.0) / (rho_inf + 1.0)
+    a_f = rho_inf / (rho_inf + 1.0)
+    gamma = 0.5 - a_m + a_f
+    return dict(b1=0.5, b2=gamma, c1=1.0 - a_f, c2=1.0 - a_f, c3=1.0 - a_m)

@@ -119,13 +119,20 @@ def _hf_amplitude_ratio(ts, w=1e4, steps=40):
     return (E[-1] / E[0]) ** (1.0 / (2 * (steps - 1)))
 
 
-def test_second_order_members_do_not_damp_high_frequencies():
-    """Reading L26: Eq. time_constraints is a Newmark update exactly when b1 = 1/2, with β = b1·b2 = γ/2,
-    γ = b2; the second-order condition of generalized-α then forces γ = 1/2, β = 1/4 — the
-    non-dissipative member.  SPEC's 'visible damping at ρ∞ = 0' is not reachable in this family:
-    the per-step amplitude at ωΔt = 1e4 is 1 for every ρ∞ knob, while a first-order member
-    (γ = b2 = 0.9) damps."""
-    for rho in (0.0, 0.5, 1.0):
-        assert _hf_amplitude_ratio(dict(dt=1.0, **ot.genalpha_rho(rho))) == pytest.approx(1.0, abs=1e-6)
-    damped = _hf_amplitude_ratio(dict(dt=1.0, b1=0.5, b2=0.9, c1=1.0, c2=1.0, c3=1.0))
-    assert damped < 0.9
+def test_genalpha_rho_damps_high_frequencies_only_below_one():
+    """SPEC S:535 (reading L26): with the ρ∞ mapping of S:412 the per-step high-frequency amplitude
+    (ωΔt = 1e4) is < 1 at ρ∞ = 0 (visible numerical damping) and exactly 1 at ρ∞ = 1 (the average-
+    acceleration member: α_m = ½, α_f = ½, γ = ½, c = ½), and it decreases monotonically with ρ∞."""
+    amp = {r: _hf_amplitude_ratio(dict(dt=1.0, **ot.genalpha_rho(r))) for r in (0.0, 0.5, 0.8, 1.0)}
+    assert amp[0.0] < 0.9
+    assert amp[1.0] == pytest.approx(1.0, abs=1e-6)
+    assert amp[0.0] < amp[0.5] < amp[0.8] < amp[1.0]
+    # and the mapping is second order at every ρ∞ (γ = ½ − α_m + α_f), measured off the extrema of cos
+    w, T = 2.0 * np.pi, 1.15
+    mats = [np.array([[w * w]]), np.zeros((1, 1)), np.array([[1.0]])]
+    for r in (0.0, 0.5, 1.0):
+        errs = []
+        for n in (80, 160, 320, 640):
+            hist = _run(dict(dt=T / n, **ot.genalpha_rho(r)), 2, mats, np.zeros(1), [[1.0], [0.0], [-w * w]], n)
+            errs.append(abs(hist[-1][0, 0] - np.cos(w * T)))
+        assert min(np.log2(errs[i] / errs[i + 1]) for i in range(3)) >= 1.9, (r, errs)
