@@ -7,7 +7,7 @@ C ABI, with the pattern + slot map prebuilt (one-time Block B, reported s
 
 Default workload: c5 = 256^3 Q1 hex linear elasticity (16,777,216 elements, 4,092,809,481 nnz),
 the config BASELINE.json quotes at 1/2/4/8 B200.  `--config cN` selects another config.
-Multi-GPU (torchrun): owner-computes partition of the control points in contiguous ranges (z-slabs)
+Multi-GPU (torchrun): owner-computes RCB partition of the control points (local numbering, owned + halo)
 with a ghost element layer; each rank writes its owned rows; the residual norms are all-reduced
 over NCCL (the D-2 convergence test); time = max over ranks (strong scaling: the mesh is fixed).
 
@@ -202,9 +202,10 @@ def main():
     mesh, prob = make_config(name, args.variant)
     state = make_state(name, mesh, prob)
     E_total = mesh.n_elems
-    if world > 1:
+    if world > 1:  # RCB part in local numbering: only owned + halo points travel to this GPU
         part = part_for_rank(mesh, world, rank)
         local_mesh, own = part.mesh, part.own
+        state = part.local_state(state)
     else:
         local_mesh, own = mesh, (0, mesh.n_nodes)
     t0 = time.perf_counter()

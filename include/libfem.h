@@ -156,7 +156,10 @@ int fem_assemble_system(fem_mesh_t mesh, fem_pattern_t pat, const fem_problem* p
                         int scatter, void* stream);
 
 /* fem_residual_norms — norms_dev[0] = Σ_i d_i², norms_dev[1] = max_i |d_i| over the κ̂·n_own owned rows
- * (the D-2 convergence test).  DEVICE output, stream-ordered. */
+ * (the D-2 convergence test).  DEVICE output, stream-ordered, no host sync.  Fixed grid (4 × SM
+ * count) and fixed summation order: bit-identical run to run on a given device.  NaN propagates into both
+ * norms (a NaN residual never passes a ‖d‖ < tol test).  Uses per-mesh scratch: calls on one mesh must
+ * not run concurrently on different streams.  Multi-GPU: all-reduce [0] with SUM and [1] with MAX. */
 int fem_residual_norms(fem_mesh_t mesh, const double* rhs, double* norms_dev, void* stream);
 
 /* fem_linearize_host — end-to-end call with HOST buffers: copies the state from (pinned) host memory
@@ -225,7 +228,8 @@ int fem_pattern_info(fem_pattern_t pat, int64_t* out8);
  * The linearisation K Δφ = -d of d(φ) = 0 is solved on the CSR of fem_pattern_build.
  *
  * fem_spmv — y = alpha·K·x + beta·y for the CSR K (rowptr int64 [n_rows+1], colidx int32 [nnz], values
- *   fp64 [nnz], all DEVICE; x, y DEVICE fp64, x indexed by column).  Stream-ordered, no sync.
+ *   fp64 [nnz], all DEVICE; x, y DEVICE fp64, x indexed by column).  Stream-ordered, no sync.  A warp owns
+ *   32 consecutive rows; the per-row sum order is fixed (bit-identical run to run).
  *   Single-GPU pattern (columns index the same vector as rows).  FEM_E_INVALID_ARG on NULL / n_rows < 0.
  *
  * fem_cg_work_doubles — size of the caller-owned DEVICE work buffer of fem_cg_solve, in doubles.
@@ -237,7 +241,9 @@ int fem_pattern_info(fem_pattern_t pat, int64_t* out8);
  *   iterations; the convergence test is read back every check_every iterations (<= 0: 16), so the call
  *   synchronizes `stream` (the only host syncs).  iters_out / relres_out (host, may be NULL) receive the
  *   iteration count and ||r||/||r_0||.  Every reduction sums in fixed order: bit-identical run to run.
- *   Errors: FEM_E_INVALID_ARG for bad arguments or a non-positive diagonal of s K (not SPD). */
+ *   A zero p·Kp or r·z freezes the iterate instead of dividing by zero.  Not converging within max_iter
+ *   is NOT an error: check relres_out against rtol.  Errors: FEM_E_INVALID_ARG for bad arguments or a
+ *   non-positive diagonal of s K (not SPD); FEM_E_NAN when the residual becomes NaN. */
 /* fem_pattern_csr — the pattern's own DEVICE CSR arrays (library-owned, valid until fem_pattern_destroy,
  *   read-only): rowptr int64 [n_rows+1], colidx int32 [nnz] (global column ids; *col_offset = own_lo, 0
  *   on a single GPU).  No copy, no sync. */
@@ -251,6 +257,10 @@ int64_t fem_bicgstab_work_doubles(int64_t n_rows);
 int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
                        const double* b, double* x, int max_iter, double rtol, int check_every, double* work,
                        int* iters_out, double* relres_out, void* stream);
+/* fem_vec_axpby — y = alpha·x + beta·y over n DEVICE doubles, each product and the sum correctly rounded
+ *   (no FMA contraction).  The Newton update φ ← φ − Δφ of D-4 and sign flips around the
+ *   solves run here, not in the binding.  Stream-ordered, no sync.  INVALID_ARG on n < 0 / NULL. */
+int fem_vec_axpby(int64_t n, double alpha, const double* x, double beta, double* y, void* stream);
 int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
              const double* x, double* y, double alpha, double beta, void* stream);
 int64_t fem_cg_work_doubles(int64_t n_rows);

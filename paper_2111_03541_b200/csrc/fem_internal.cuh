@@ -130,6 +130,11 @@ struct fem_mesh_s {
   std::vector<std::vector<int8_t>> h_bset_facet;
   std::vector<std::vector<uint8_t>> h_bset_colour;
   long long* err = nullptr;     // device error word: an offending element id or -1
+  // fixed-order residual norms: per-block partials (Σd², max|d|) + the last-block ticket; sized for
+  // norm_blocks = 4 × the device's SM count (queried at create), so the reduction order is fixed per device
+  double* norm_partials = nullptr;
+  unsigned int* norm_ticket = nullptr;
+  int norm_blocks = 0;
   double* scratch_state = nullptr;  // e2e staging buffer (lazily allocated)
   size_t scratch_state_bytes = 0;
   // pipelined e2e (fem_linearize_host_async): two staging buffers, a copy stream and their events

@@ -107,6 +107,8 @@ void fem_mesh_destroy(fem_mesh_t m) {
   for (auto p : m->bset_elem_dev) cudaFree(p);
   for (auto p : m->bset_facet_dev) cudaFree(p);
   cudaFree(m->err);
+  cudaFree(m->norm_partials);
+  cudaFree(m->norm_ticket);
   if (m->scratch_state) cudaFree(m->scratch_state);
   for (int b = 0; b < 2; b++) {
     if (m->async_state[b]) cudaFree(m->async_state[b]);
@@ -171,6 +173,15 @@ int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const dou
   MTRY(cudaMalloc(&m->coords, sizeof(double) * dim * n_nodes));
   MTRY(cudaMalloc(&m->conn, sizeof(int32_t) * nl * (n_elems > 0 ? n_elems : 1)));
   MTRY(cudaMalloc(&m->err, sizeof(long long)));
+  {
+    int dev = 0, sms = 0;
+    MTRY(cudaGetDevice(&dev));
+    MTRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    m->norm_blocks = 4 * (sms > 0 ? sms : 1);
+  }
+  MTRY(cudaMalloc(&m->norm_partials, sizeof(double) * 2 * m->norm_blocks));
+  MTRY(cudaMalloc(&m->norm_ticket, sizeof(unsigned int)));
+  MTRY(cudaMemsetAsync(m->norm_ticket, 0, sizeof(unsigned int), s));
   MTRY(cudaMemcpyAsync(m->coords, coords, sizeof(double) * dim * n_nodes, cudaMemcpyHostToDevice, s));
   if (n_elems > 0) MTRY(cudaMemcpyAsync(m->conn, conn, sizeof(int32_t) * nl * n_elems, cudaMemcpyHostToDevice, s));
   MTRY(cudaMemsetAsync(m->err, 0xff, sizeof(long long), s));

@@ -196,40 +196,65 @@ int pattern_build(fem_mesh_s* m, cudaStream_t s, fem_pattern_s* p) {
 }
 
 // ---------------------------------------------------------------- residual norms (P:439 check)
-__global__ void k_norms(const double* __restrict__ d, int64_t n, double* __restrict__ out) {
+// max|·| that propagates NaN (fmax drops it): an all-NaN residual must not pass a ‖d‖∞ < atol test.
+__device__ __forceinline__ double nanmax_abs(double m, double v) {
+  const double a = fabs(v);
+  return (a != a || m != m || a > m) ? (m != m ? m : a) : m;
+}
+
+// Σd² and max|d| over n entries with a fixed grid (norm_blocks = 4 × SMs) and a fixed summation order:
+// thread t of block b reads i = b·NT + t + k·(grid·NT) in order, then a fixed xor tree, warp totals in warp
+// order, and the last-arriving block sums the block partials 0..grid-1 in order — bit-reproducible run to run
+// (the round-1 kernel combined blocks with a global atomicAdd, whose order varied).
+constexpr int NORM_NT = 256;
+__global__ void __launch_bounds__(NORM_NT) k_norms(const double* __restrict__ d, int64_t n,
+                                                   double* __restrict__ partials, unsigned int* __restrict__ ticket,
+                                                   double* __restrict__ out) {
+  __shared__ double ss[NORM_NT / 32], sm[NORM_NT / 32];
+  __shared__ bool last;
   double s = 0.0, mx = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = d[i];
-    s += v * v;
-    mx = fmax(mx, fabs(v));
+  for (int64_t i = blockIdx.x * (int64_t)NORM_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NORM_NT) {
+    const double v = __ldcs(d + i);
+    s = fma(v, v, s);
+    mx = nanmax_abs(mx, v);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, o);
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mx = nanmax_abs(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  __shared__ double ss[32], sm[32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) { ss[w] = s; sm[w] = mx; }
   __syncthreads();
-  if (w == 0) {
-    s = (l < (int)(blockDim.x >> 5)) ? ss[l] : 0.0;
-    mx = (l < (int)(blockDim.x >> 5)) ? sm[l] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (threadIdx.x == 0) {
+    double b = 0.0, bm = 0.0;
+    for (int k = 0; k < NORM_NT / 32; k++) { b += ss[k]; bm = nanmax_abs(bm, sm[k]); }
+    partials[2 * blockIdx.x] = b;
+    partials[2 * blockIdx.x + 1] = bm;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double b = 0.0, bm = 0.0;
+    for (unsigned k = 0; k < gridDim.x; k++) {
+      b += __ldcg(partials + 2 * k);
+      bm = nanmax_abs(bm, __ldcg(partials + 2 * k + 1));
     }
-    if (l == 0) {
-      atomicAdd(out, s);
-      // max of non-negative doubles via their ordered int64 bit patterns
-      atomicMax((unsigned long long*)(out + 1), (unsigned long long)__double_as_longlong(mx));
-    }
+    out[0] = b;
+    out[1] = bm;
+    *ticket = 0u;
   }
 }
 
 int residual_norms(const fem_mesh_s* m, const double* rhs, double* norms, cudaStream_t s) {
-  FEM_CUDA_TRY(cudaMemsetAsync(norms, 0, 2 * sizeof(double), s));
   const int64_t n = (int64_t)m->kh * m->n_own;
-  if (n > 0) k_norms<<<grid_for(n) > 148 * 4 ? 148 * 4 : grid_for(n), 256, 0, s>>>(rhs, n, norms);
+  if (n <= 0) {
+    FEM_CUDA_TRY(cudaMemsetAsync(norms, 0, 2 * sizeof(double), s));
+    return 0;
+  }
+  k_norms<<<m->norm_blocks, NORM_NT, 0, s>>>(rhs, n, m->norm_partials, m->norm_ticket, norms);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(SV_THREADS) k_cg_spmv(int64_t n, const int64_t
   if (block_reduce_last(dot, partials, &sc->count0, &pq)) {
     sc->pq = pq;
     sc->rz = sc->rz_new;  // every block of the previous k_cg_dir has used the old rz (stream order)
-    sc->alpha = sc->rz / pq;
+    // breakdown guard: p·q = 0 (p = 0 after exact convergence inside a check block, or a zero-energy
+    // direction) leaves x unchanged instead of spreading 0/0 into it
+    sc->alpha = pq != 0.0 ? sc->rz / pq : 0.0;
   }
 }
 
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(SV_THREADS) k_cg_update(int64_t n, double* __r
 // p = z + β p with β = rz_new / rz (rz ← rz_new happens in the next k_cg_spmv)
 __global__ void __launch_bounds__(SV_THREADS) k_cg_dir(int64_t n, const double* __restrict__ z, double* __restrict__ p,
                                                        CgScal* sc, int first) {
-  const double beta = first ? 0.0 : sc->rz_new / sc->rz;
+  const double beta = (first || sc->rz == 0.0) ? 0.0 : sc->rz_new / sc->rz;
   for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS)
     p[i] = first ? z[i] : fma(beta, p[i], z[i]);
 }
@@ -284,134 +286,6 @@ __global__ void __launch_bounds__(SV_THREADS) k_cg_init(int64_t n, const int64_t
     sc->rr0 = out;
   }
 }
-
-// ---- TMA-staged SpMV (opt-in, FEM_SPMV_TMA=1): persistent CTAs (two per SM) walk chunks of SP_ROWS rows;
-// the chunk's values and column indices (contiguous in the CSR) arrive by two cp.async.bulk copies into a
-// 3-stage shared-memory ring while an earlier chunk is computed.  Measured on c5 it reaches 2.7 TB/s
-// (18.4 ms) against 3.9 TB/s (12.8 ms) for the per-row kernel: the per-chunk compute (rowptr loads, then
-// the x gathers from L2) is serial per CTA and does not hide behind the copies; kept as a tested
-// variant for the next round (stage rowptr with the chunk, overlap more chunks per SM).
-constexpr int SP_ROWS = 32;           // rows per chunk
-constexpr int SP_THREADS = 256;     // 8 warps x 4 rows (8 lanes each) = SP_ROWS; two CTAs per SM
-static_assert(SP_THREADS / 32 * 4 == SP_ROWS, "one pass of the warps covers a chunk");
-constexpr int SP_CAP = 32 * 81 + 16;  // entries per stage (≥ SP_ROWS × largest row + alignment slack)
-constexpr int SP_STAGES = 3;          // chunks in flight: two stream in while one is computed
-
-__device__ __forceinline__ uint32_t sv_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void sv_mbar_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sv_smem(b)) : "memory");
-}
-__device__ __forceinline__ void sv_expect(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sv_smem(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void sv_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sv_smem(dst)),
-               "l"(src), "r"(bytes), "r"(sv_smem(b))
-               : "memory");
-}
-__device__ __forceinline__ void sv_wait(uint64_t* b, uint32_t parity) {
-  asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
-                   sv_smem(b)),
-               "r"(parity)
-               : "memory");
-}
-
-struct SpChunk {  // 16-byte aligned copy windows of chunk rows [r0, r1)
-  int64_t k0, kv, kc;  // first entry, aligned value start (kv <= k0), aligned column start (kc <= k0)
-  uint32_t vbytes, cbytes;
-};
-__device__ __forceinline__ SpChunk sp_chunk(const int64_t* rowptr, int64_t r0, int64_t r1) {
-  SpChunk c;
-  c.k0 = rowptr[r0];
-  const int64_t k1 = rowptr[r1];
-  c.kv = c.k0 & ~int64_t(1);
-  c.kc = c.k0 & ~int64_t(3);
-  c.vbytes = (uint32_t)(((k1 - c.kv) * 8 + 15) & ~int64_t(15));
-  c.cbytes = (uint32_t)(((k1 - c.kc) * 4 + 15) & ~int64_t(15));
-  return c;
-}
-
-// MODE 0: y = alpha K x + beta y.  MODE 1 (CG): q = s K p and p·q (last block forms α, as k_cg_spmv).
-template <int MODE>
-__global__ void __launch_bounds__(SP_THREADS, 2) k_spmv_tma(int64_t n, const int64_t* __restrict__ rowptr,
-                                                           const int32_t* __restrict__ colidx,
-                                                           const double* __restrict__ val, const double* __restrict__ x,
-                                                           double* __restrict__ y, double alpha, double beta,
-                                                           double* partials, CgScal* sc) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
-  auto vbuf = [&](int b) { return reinterpret_cast<double*>(sm + 64 + (size_t)12 * SP_CAP * b); };
-  auto cbuf = [&](int b) { return reinterpret_cast<int32_t*>(sm + 64 + (size_t)12 * SP_CAP * b + 8 * SP_CAP); };
-  const int64_t nch = (n + SP_ROWS - 1) / SP_ROWS;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < SP_STAGES; b++) sv_mbar_init(&bar[b]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t ch, int b) {
-    const int64_t r0 = ch * SP_ROWS, r1 = min(n, r0 + SP_ROWS);
-    const SpChunk c = sp_chunk(rowptr, r0, r1);
-    if (c.vbytes > 8u * SP_CAP || c.cbytes > 4u * SP_CAP) {  // oversize chunk: computed from global memory
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sv_smem(&bar[b])) : "memory");
-      return;
-    }
-    sv_expect(&bar[b], c.vbytes + c.cbytes);
-    sv_bulk(vbuf(b), val + c.kv, c.vbytes, &bar[b]);
-    sv_bulk(cbuf(b), colidx + c.kc, c.cbytes, &bar[b]);
-  };
-  int64_t ch = blockIdx.x;
-  if (threadIdx.x == 0)
-    for (int k = 0; k < SP_STAGES - 1; k++)
-      if (ch + (int64_t)k * gridDim.x < nch) issue(ch + (int64_t)k * gridDim.x, k);
-  double dot = 0.0;
-  for (int it = 0; ch < nch; it++, ch += gridDim.x) {
-    const int b = it % SP_STAGES;
-    const int64_t ahead = ch + (int64_t)(SP_STAGES - 1) * gridDim.x;
-    // stage (it + SP_STAGES - 1) % SP_STAGES was freed by the last barrier
-    if (threadIdx.x == 0 && ahead < nch) issue(ahead, (it + SP_STAGES - 1) % SP_STAGES);
-    sv_wait(&bar[b], (uint32_t)((it / SP_STAGES) & 1));
-    const int64_t r0 = ch * SP_ROWS, r1 = min(n, r0 + SP_ROWS);
-    const SpChunk c = sp_chunk(rowptr, r0, r1);
-    const bool staged = c.vbytes <= 8u * SP_CAP && c.cbytes <= 4u * SP_CAP;
-    const double* vb = staged ? vbuf(b) - c.kv : val;      // entry k at vb[k]
-    const int32_t* cb = staged ? cbuf(b) - c.kc : colidx;  // (pointer offsets only, never dereferenced outside)
-    {  // 8 lanes per row, the 64 rows of the chunk in one pass of the 16 warps: every lane's loads and
-       // x gathers are independent (unrolled), so a chunk costs about one L2 round trip
-      const int64_t r = r0 + warp * 4 + (lane >> 3);
-      const int sub = lane & 7;
-      double acc = 0.0;
-      if (r < r1) {
-        const int64_t a = rowptr[r], e = rowptr[r + 1];
-        int64_t k = a + sub;
-#pragma unroll 4
-        for (; k < e; k += 8) acc = fma(vb[k], __ldg(x + cb[k]), acc);
-      }
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 8);
-      if (sub == 0 && r < r1) {
-        if (MODE == 0) {
-          y[r] = alpha * acc + (beta == 0.0 ? 0.0 : beta * y[r]);
-        } else {
-          const double qr = alpha * acc;  // alpha carries s
-          y[r] = qr;
-          dot = fma(x[r], qr, dot);
-        }
-      }
-    }
-    __syncthreads();  // every warp is done with buffer b before it is refilled
-  }
-  if (MODE == 1) {
-    double pq;
-    if (block_reduce_last<SP_THREADS>(dot, partials, &sc->count0, &pq)) {
-      sc->pq = pq;
-      sc->rz = sc->rz_new;
-      sc->alpha = sc->rz / pq;
-    }
-  }
-}
-
-static size_t spmv_tma_smem() { return 64 + (size_t)12 * SP_CAP * SP_STAGES; }
 
 // ---- Jacobi-preconditioned BiCGStab (van der Vorst) for the non-symmetric systems: the thermal FIX term
 // k N_a n·∇T and the NS forms make K non-symmetric, so CG does not apply.
@@ -541,22 +415,11 @@ __global__ void __launch_bounds__(SV_THREADS) k_bi_init(int64_t n, const int64_t
   }
 }
 
-// lanes per CSR row of the SpMV kernels (FEM_SPMV_LANES = 8 | 16 | 32 for A/B runs)
-static int spmv_lanes() {
-  const char* e = getenv("FEM_SPMV_LANES");
-  const int g = e ? atoi(e) : 0;  // c5: warp-owned 32-row blocks 11.4 ms; 32 lanes/row 12.8, 16: 13.8, 8: 14.6 ms
-  return (g == 0 || g == 16 || g == 32) ? g : 8;
-}
-
-// Row mapping for the solvers' SpMVs from the average row length (one 8-byte read + sync at solve start,
-// next to the init sync the solvers already do): long rows (Q1 elasticity, 81) take the warp-owned
-// 32-row blocks, short rows (scalar Q1, 27) 8 lanes per row (c2 transient: 8 lanes beat the row blocks
-// by 7%).  FEM_SPMV_LANES overrides.
+// Row mapping of the SpMV kernels from the average row length (one 8-byte read + sync, next to the init
+// sync the solvers already do): long rows (Q1 elasticity, 81 entries) take the warp-owned 32-row blocks
+// (c5: 11.4 ms vs 12.8 for 32 lanes per row, 14.6 for 8), short rows (scalar Q1, 27) 8 lanes per row
+// (c2 transient: 7% faster than the row blocks).
 static int solver_lanes(const int64_t* rowptr, int64_t n, cudaStream_t s, int* g) {
-  if (getenv("FEM_SPMV_LANES")) {
-    *g = spmv_lanes();
-    return 0;
-  }
   int64_t nnz = 0;
   FEM_CUDA_TRY(cudaMemcpyAsync(&nnz, rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   FEM_CUDA_TRY(cudaStreamSynchronize(s));
@@ -580,23 +443,27 @@ extern "C" int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* co
     return FEM_E_INVALID_ARG;
   }
   if (n_rows == 0) return 0;
-  if (getenv("FEM_SPMV_TMA")) {  // TMA-staged chunks (opt-in: 18.4 ms vs 12.8 ms for the row kernel on c5)
-    static bool attr = false;
-    if (!attr) {
-      FEM_CUDA_TRY(cudaFuncSetAttribute(k_spmv_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spmv_tma_smem()));
-      attr = true;
-    }
-    const int64_t nch = (n_rows + SP_ROWS - 1) / SP_ROWS;
-    k_spmv_tma<0><<<(unsigned)std::min<int64_t>(nch, 2 * 148), SP_THREADS, spmv_tma_smem(), (cudaStream_t)stream>>>(
-        n_rows, rowptr, colidx, values, x, y, alpha, beta, nullptr, nullptr);
-    FEM_CUDA_TRY(cudaGetLastError());
-    return 0;
+  // no host sync here (the solvers pick the row mapping from the average row length): warp-owned 32-row blocks
+  k_spmv<0><<<grid_for(n_rows, 1), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// y = alpha x + beta y, each product and the sum correctly rounded (no FMA contraction): the Newton update
+// φ ← φ - Δ of D-4 and the sign flips around the solves, done in the library not the binding.
+__global__ void __launch_bounds__(SV_THREADS) k_axpby(int64_t n, double alpha, const double* __restrict__ x, double beta,
+                                                      double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * SV_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * SV_THREADS)
+    y[i] = __dadd_rn(__dmul_rn(alpha, x[i]), __dmul_rn(beta, y[i]));
+}
+
+extern "C" int fem_vec_axpby(int64_t n, double alpha, const double* x, double beta, double* y, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) {
+    set_error("fem_vec_axpby: invalid argument");
+    return FEM_E_INVALID_ARG;
   }
-  const int g = spmv_lanes();
-  if (g == 0) k_spmv<0><<<grid_for(n_rows, 1), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
-  else if (g == 32) k_spmv<32><<<grid_for(n_rows, 32), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
-  else if (g == 16) k_spmv<16><<<grid_for(n_rows, 16), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
-  else k_spmv<8><<<grid_for(n_rows, 8), SV_THREADS, 0, (cudaStream_t)stream>>>(n_rows, rowptr, colidx, values, x, y, alpha, beta);
+  if (n == 0) return 0;
+  k_axpby<<<grid_for(n, 1), SV_THREADS, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -627,9 +494,6 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
   int g = 0;
   if (int rc = solver_lanes(rowptr, n, s, &g)) return rc;
   const int gv = grid_for(n, 1), gm = grid_for(n, g ? g : 1);
-  const bool tma = getenv("FEM_SPMV_TMA") != nullptr;
-  const int gt = (int)std::min<int64_t>((n + SP_ROWS - 1) / SP_ROWS, 2 * 148);
-  if (tma) FEM_CUDA_TRY(cudaFuncSetAttribute(k_spmv_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spmv_tma_smem()));
   k_cg_init<<<gv, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, b, x, r, z, dinv, partials, sc, bad);
   k_cg_dir<<<gv, SV_THREADS, 0, s>>>(n, z, p, sc, 1);
   FEM_CUDA_TRY(cudaGetLastError());
@@ -649,10 +513,7 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
   while (rr0 > 0.0 && it < max_iter && rel > rtol) {
     const int todo = std::min(chk, max_iter - it);
     for (int k = 0; k < todo; k++) {
-      if (tma) k_spmv_tma<1><<<gt, SP_THREADS, spmv_tma_smem(), s>>>(n, rowptr, colidx, values, p, q, spd_sign, 0.0, partials, sc);
-      else if (g == 0) k_cg_spmv<0><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
-      else if (g == 32) k_cg_spmv<32><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
-      else if (g == 16) k_cg_spmv<16><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
+      if (g == 0) k_cg_spmv<0><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
       else k_cg_spmv<8><<<gm, SV_THREADS, 0, s>>>(n, rowptr, colidx, values, spd_sign, p, q, partials, sc);
       k_cg_update<<<gv, SV_THREADS, 0, s>>>(n, x, r, p, q, dinv, z, partials, sc);
       k_cg_dir<<<gv, SV_THREADS, 0, s>>>(n, z, p, sc, 0);
@@ -662,6 +523,12 @@ extern "C" int fem_cg_solve(int64_t n_rows, const int64_t* rowptr, const int32_t
     FEM_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof(CgScal), cudaMemcpyDeviceToHost, s));
     FEM_CUDA_TRY(cudaStreamSynchronize(s));
     rel = sqrt(h.rr / rr0);
+    if (!(rel == rel)) {
+      set_error("fem_cg_solve: breakdown (NaN in the recurrence)");
+      if (iters_out) *iters_out = it;
+      if (relres_out) *relres_out = rel;
+      return FEM_E_NAN;
+    }
   }
   if (iters_out) *iters_out = it;
   if (relres_out) *relres_out = rel;
@@ -718,8 +585,6 @@ extern "C" int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const i
       k_bi_dir<<<gv, SV_THREADS, 0, st>>>(n, r, p, v, dinv, y, sc, it + k == 0);
 #define BI_SPMV(MODE, IN, OUT, A)                                                                                 \
   if (g == 0) k_bi_spmv<0, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
-  else if (g == 32) k_bi_spmv<32, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
-  else if (g == 16) k_bi_spmv<16, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc); \
   else k_bi_spmv<8, MODE><<<gm, SV_THREADS, 0, st>>>(n, rowptr, colidx, values, IN, OUT, A, partials, sc);
       BI_SPMV(0, y, v, rh)
       k_bi_half<<<gv, SV_THREADS, 0, st>>>(n, x, y, r, v, dinv, sv, z, sc);

@@ -131,6 +131,7 @@ def lib():
         L.fem_mesh_destroy.restype = None
         L.fem_pattern_csr.argtypes = [V, C.POINTER(V), C.POINTER(V), C.POINTER(I64)]
         L.fem_spmv.argtypes = [I64, V, V, V, V, V, C.c_double, C.c_double, V]
+        L.fem_vec_axpby.argtypes = [I64, C.c_double, V, C.c_double, V, V]
         L.fem_cg_work_doubles.argtypes = [I64]
         L.fem_cg_work_doubles.restype = I64
         L.fem_cg_solve.argtypes = [I64, V, V, V, V, V, C.c_double, I, C.c_double, I, V, C.POINTER(I),
@@ -154,7 +155,7 @@ EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pa
             "fem_linearize_host", "fem_linearize_host_async", "fem_pattern_export_coo", "fem_gather", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
             "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve",
-            "fem_time_init", "fem_time_effective", "fem_time_increment"]
+            "fem_time_init", "fem_time_effective", "fem_time_increment", "fem_vec_axpby"]
 
 
 def _check(rc):
@@ -271,6 +272,11 @@ def fem_pattern_csr(pat_h):
 def fem_spmv(n_rows, rowptr, colidx, values, x, y, alpha=1.0, beta=0.0, stream=None):
     _check(lib().fem_spmv(int(n_rows), _ptr(rowptr), _ptr(colidx), _ptr(values), _ptr(x), _ptr(y), float(alpha),
                           float(beta), _stream(stream)))
+
+
+def fem_vec_axpby(n, alpha, x, beta, y, stream=None):
+    """y = alpha x + beta y on the device (fem_vec_axpby)."""
+    _check(lib().fem_vec_axpby(int(n), float(alpha), _ptr(x), float(beta), _ptr(y), _stream(stream)))
 
 
 def fem_cg_work_doubles(n_rows):

@@ -1,5 +1,8 @@
-"""FemSystem — torch-tensor convenience wrapper over the libfem C ABI (no compute here)."""
+"""FemSystem — torch-tensor convenience wrapper over the libfem C ABI (no compute here: every step of
+the method, including the Newton update and the convergence norms, runs in libfem.so)."""
 from __future__ import annotations
+
+import math
 
 import torch
 
@@ -122,13 +125,22 @@ class FemSystem:
         fem.fem_spmv(self.n_rows, rp, ci, self.values, x, y, alpha, beta)
         return y
 
+    def _solve_checked(self, d, method, spd_sign, rtol, max_iter):
+        """Solve K y = d (y = -Δφ of D-4) and reject a NaN / non-converged solve (returns y, it, rel)."""
+        y, it, rel = self.solve(d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method)
+        if not math.isfinite(rel):
+            raise fem.FemError(-5, f"linear solve broke down (relative residual {rel})")
+        return y, it, rel
+
     def newton_step(self, state, scatter="tiled", spd_sign=-1.0, rtol=1e-12, max_iter=20000, method="cg"):
         """One Newton sub-step (D-1..D-4) for a static problem: assemble K and d at φ, solve
-        K Δφ = -d, return φ + Δφ (state level 0), the solver iterations and relative residual."""
+        K Δφ = -d as K y = d, φ ← φ - y (fem_vec_axpby).  Returns the new state (level 0
+        updated), the solver iterations and the relative residual ||r||/||r0|| (compare with rtol: hitting
+        max_iter is reported, not raised; a NaN raises FemError)."""
         K, d = self.system(state, scatter=scatter)
-        dx, it, rel = self.solve(-d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method)
+        y, it, rel = self._solve_checked(d, method, spd_sign, rtol, max_iter)
         new = state.clone()
-        new[0] += dx.view(self.kh, self.N)
+        fem.fem_vec_axpby(self.kh * self.N, -1.0, y, 1.0, new[0])
         return new, it, rel
 
     # ---- NEXT-3: one generalized-alpha timestep (Blocks C and D, P:404-465) on the GPU
@@ -137,8 +149,9 @@ class FemSystem:
         """Advance one timestep with the problem's generalized-alpha scheme, in place on the DEVICE arrays
         phi0 (committed ∂^ν φ) and incr (Δ∂^ν φ), both float64 [ν̂+1][κ̂][N].  Block C (fem_time_init,
         fused with the first D-1), then up to n_sub sub-steps: assemble K, d at the effective values (D-2,
-        D-3), solve K Δ_sub = -d (D-4, fem_cg/bicgstab), fem_time_increment (fused with the next D-1);
-        stops early when ||d||_2 <= tol.  Returns the list of (||d||_2 before the solve, iterations)."""
+        D-3), the D-2 test ||d||_2 <= tol (fem_residual_norms), solve K y = d (D-4, CG/BiCGStab), Δ_sub = -y
+        (fem_vec_axpby), fem_time_increment (fused with the next D-1).  Returns the list of
+        (||d||_2 before the solve, iterations, relative solver residual)."""
         t = self.problem.time
         if t.kind != "genalpha":
             raise ValueError("time_step needs a genalpha problem")
@@ -151,13 +164,14 @@ class FemSystem:
         hist = []
         for _ in range(n_sub):
             K, d = self.system(eff, scatter=scatter)
-            dn = float(torch.linalg.vector_norm(d))
+            dn = math.sqrt(float(self.norms(d)[0]))
             if dn <= tol:
-                hist.append((dn, 0))
+                hist.append((dn, 0, 0.0))
                 break
-            dx, it, _ = self.solve(-d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method)
-            fem.fem_time_increment(ts, n, dx, incr, phi0, eff)
-            hist.append((dn, it))
+            y, it, rel = self._solve_checked(d, method, spd_sign, rtol, max_iter)
+            fem.fem_vec_axpby(n, 0.0, y, -1.0, y)   # Δ_sub = -y
+            fem.fem_time_increment(ts, n, y, incr, phi0, eff)
+            hist.append((dn, it, rel))
         return hist
 
     def norms(self, rhs=None):

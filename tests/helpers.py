@@ -77,3 +77,28 @@ def rhs_err(d_test, d_ref, abs_d):
     den = np.maximum(np.abs(d_ref), abs_d)
     den = np.where(den > 0, den, 1.0)
     return float((np.abs(d_test - d_ref) / den).max()) if len(d_ref) else 0.0
+
+
+def part_csr_to_global(part, rowptr, colidx, values, kh, n_global):
+    """A partitioned rank's CSR (local relabelling, paper.partition) as global rows: returns
+    (global row ids, rowptr, global colidx sorted within each row, values permuted alike).  Index
+    bookkeeping only (the relabelling of paper_2111_03541_b200/partition.py)."""
+    rows = part.global_rows(kh, n_global)
+    cols = part.global_cols(colidx, n_global)
+    out_c = np.empty_like(cols)
+    out_v = np.empty_like(values)
+    for r in range(len(rows)):
+        a, b = rowptr[r], rowptr[r + 1]
+        o = np.argsort(cols[a:b], kind="stable")
+        out_c[a:b] = cols[a:b][o]
+        out_v[a:b] = values[a:b][o]
+    return rows, rowptr, out_c, out_v
+
+
+def scatter_rows_into(full_rowptr, full_colidx, rows, rowptr, cols, vals, dst):
+    """Place a part's global-row CSR into a full-size values array after checking that every row's global
+    columns equal the full pattern's row (pattern bit-exact)."""
+    for r, g in enumerate(rows):
+        a, b = full_rowptr[g], full_rowptr[g + 1]
+        np.testing.assert_array_equal(cols[rowptr[r]:rowptr[r + 1]], full_colidx[a:b])
+        dst[a:b] = vals[rowptr[r]:rowptr[r + 1]]

@@ -206,52 +206,37 @@ def test_inverted_element_reported_and_edge_cases():
     S.close()
 
 
-def _partition_rows(m, nparts):
-    """Contiguous owned node ranges + elements touching them (the multi-GPU partition)."""
-    from paper_2111_03541_b200.partition import partition_nodes
-    return partition_nodes(m, nparts)
-
-
-@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
-def test_partitioned_owned_rows_equal_single(name):
-    """Each part assembles only its owned rows (owner computes, one ghost element layer); the
-    concatenated parts reproduce the single-GPU pattern bit-exactly and values within L20."""
+@pytest.mark.parametrize("name,variant", [("c2", "structured"), ("c4", "perturbed"), ("c5", "structured"),
+                                          ("c5", "perturbed")])
+def test_partitioned_owned_rows_equal_single(name, variant):
+    """Each RCB part (local relabelling: owned points, then halo points; partition.py) assembles only its
+    owned rows (owner computes, one ghost element layer) from its LOCAL coordinates and state; mapped back
+    through node_ids the parts reproduce the single-GPU pattern bit-exactly and values within L20."""
     _need_gpu()
+    from helpers import part_csr_to_global, scatter_rows_into
     from paper_2111_03541_b200 import FemSystem
-    m, p = make_config(name, "structured", SMALL[name])
+    from paper_2111_03541_b200.partition import partition_nodes
+    m, p = make_config(name, variant, SMALL[name])
     st = make_state(name, m, p)
     ora = oracle.assemble(m, p, st)
-    full = FemSystem(m, p)
-    fp = full.export_pattern(slot=False)
-    sd = _to_dev(st)
-    parts = _partition_rows(m, 3)
+    parts = partition_nodes(m, 3)
     kh = p.kappa_hat(m.dim)
-    N = m.n_nodes
     for sc in SCATTERS:
-        got_v = np.zeros(full.nnz)
-        got_r = np.zeros(full.n_rows)
+        got_v = np.full(len(ora["values"]), np.nan)
+        got_r = np.full(len(ora["rhs"]), np.nan)
         for part in parts:
             S = FemSystem(part.mesh, p, own=part.own)
-            v, r = S.system(sd, scatter=sc)
+            v, r = S.system(_to_dev(part.local_state(st)), scatter=sc)
             pp = S.export_pattern(slot=False)
-            lo, hi = part.own
-            rp_full = fp["rowptr"].cpu().numpy()
-            rp = pp["rowptr"].cpu().numpy()
-            ci = pp["colidx"].cpu().numpy()
-            vv = v.cpu().numpy()
-            rr = r.cpu().numpy()
-            n_own = hi - lo
-            for k0 in range(kh):
-                g0, g1 = k0 * N + lo, k0 * N + hi
-                a, b = rp_full[g0], rp_full[g1]
-                la, lb = rp[k0 * n_own], rp[(k0 + 1) * n_own]
-                np.testing.assert_array_equal(ci[la:lb], fp["colidx"][a:b].cpu().numpy())
-                got_v[a:b] = vv[la:lb]
-                got_r[g0:g1] = rr[k0 * n_own:(k0 + 1) * n_own]
+            rows, rp, cols, vals = part_csr_to_global(part, pp["rowptr"].cpu().numpy(), pp["colidx"].cpu().numpy(),
+                                                      v.cpu().numpy(), kh, m.n_nodes)
+            scatter_rows_into(ora["rowptr"], ora["colidx"], rows, rp, cols, vals, got_v)
+            got_r[rows] = r.cpu().numpy()
+            assert S.status() == (0, -1)
             S.close()
-        assert csr_row_scaled_err(ora["rowptr"], got_v, ora["values"]) <= TOL
-        assert rhs_err(got_r, ora["rhs"], ora["abs_d"]) <= TOL
-    full.close()
+        assert not np.isnan(got_v).any() and not np.isnan(got_r).any()
+        assert csr_row_scaled_err(ora["rowptr"], got_v, ora["values"]) <= TOL, sc
+        assert rhs_err(got_r, ora["rhs"], ora["abs_d"]) <= TOL, sc
 
 
 FULL_SAMPLES = 160

@@ -43,7 +43,7 @@ def main():
     iters = []
     e0.record()
     for _ in range(steps):
-        iters.append([it for _, it in S.time_step(phi0, incr, n_sub=n_sub, rtol=1e-10)])
+        iters.append([h[1] for h in S.time_step(phi0, incr, n_sub=n_sub, rtol=1e-10)])
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
