@@ -13,7 +13,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .meshgen import Mesh, facets_on_plane, hex_box, perturb_and_permute, tet_box, tri_square
+from .meshgen import Mesh, facets_on_plane, hex_box, hex_box_quadratic, perturb_and_permute, tet_box, tri_square
 
 SIGMA_B = 5.670e-8  # Stefan-Boltzmann constant as printed at P:827
 
@@ -65,6 +65,10 @@ CONFIGS = {
     "c3": ConfigSpec("c3", 3, (230, 23, 23), "3D elasticity cantilever [0,10]x[0,1]^2, Kuhn P2 tets"),
     "c4": ConfigSpec("c4", 4, (451, 74, 74), "3D SUPG/PSPG Navier-Stokes channel, Kuhn P1/P1 tets"),
     "c5": ConfigSpec("c5", 5, (256, 256, 256), "3D elasticity, 256^3 Q1 hex"),
+    # NEXT-2: the quadratic cubes of the paper's experiments
+    "q2": ConfigSpec("q2", 6, (160, 16, 16), "3D elasticity cantilever [0,10]x[0,1]^2, 27-node Q2 hex"),
+    "s2": ConfigSpec("s2", 7, (160, 16, 16), "3D elasticity cantilever [0,10]x[0,1]^2, 20-node serendipity hex"),
+    "q2ns": ConfigSpec("q2ns", 8, (60, 10, 10), "3D SUPG/PSPG Navier-Stokes channel, 27-node Q2 hex"),
 }
 
 
@@ -152,6 +156,36 @@ def _problem_and_mesh(name: str, dims):
                  Term("ELAST_LOAD", 1, dict(sigma_l=tuple(sl)))]
         prob = Problem("elasticity", "hex", 1, 2, terms)
         h = (1.0 / nx, 1.0 / ny, 1.0 / nz)
+    elif name in ("q2", "s2"):
+        nx, ny, nz = dims
+        L, hh = 10.0, 1.0
+        mesh = hex_box_quadratic(nx, ny, nz, L, hh, hh, serendipity=(name == "s2"))
+        mesh.bsets = [facets_on_plane(mesh, 0, 0.0), facets_on_plane(mesh, 0, L)]
+        mesh.bset_names = ["x0_fix", "xL_load"]
+        P = 1e-3
+        sl = [0.0] * 9
+        sl[3 * 1 + 0] = -P / hh ** 2
+        terms = [Term("ELAST_DOMAIN", -1, dict(E=1.0, nu=0.3)),
+                 Term("ELAST_FIX_ALL", 0, dict(tau=1e3, dw=(0.0, 0.0, 0.0))),
+                 Term("ELAST_LOAD", 1, dict(sigma_l=tuple(sl)))]
+        prob = Problem("elasticity", mesh.etype, 2, 3, terms)
+        h = (L / nx, hh / ny, hh / nz)
+    elif name == "q2ns":
+        nx, ny, nz = dims
+        L, H = 2.5, 0.41
+        mesh = hex_box_quadratic(nx, ny, nz, L, H, H)
+        walls = _merge([facets_on_plane(mesh, 1, 0.0), facets_on_plane(mesh, 1, H),
+                        facets_on_plane(mesh, 2, 0.0), facets_on_plane(mesh, 2, H)])
+        mesh.bsets = [facets_on_plane(mesh, 0, 0.0), facets_on_plane(mesh, 0, L), walls]
+        mesh.bset_names = ["inflow", "outflow", "walls"]
+        rho, mu, U = 1000.0, 1.0, 0.45
+        tau_m, tau_c, tau_b = ns_tau(rho, mu, U, H / ny)
+        terms = [Term("NS_DOMAIN", -1, dict(rho=rho, mu=mu, tau_m=tau_m, tau_c=tau_c)),
+                 Term("NS_BND_INFLOW", 0, dict(rho=rho, mu=mu, tau_b=tau_b, U=U, H=H)),
+                 Term("NS_BND_OUTFLOW", 1, dict(rho=rho, mu=mu)),
+                 Term("NS_BND_FIX", 2, dict(rho=rho, mu=mu, tau_b=tau_b))]
+        prob = Problem("ns", "hex", 2, 3, terms)
+        h = (L / nx, H / ny, H / nz)
     else:
         raise KeyError(name)
     return mesh, prob, h
@@ -172,7 +206,7 @@ def make_config(name: str, variant: str = "structured", dims=None):
     mesh, prob, h = _problem_and_mesh(name, dims)
     if variant == "perturbed":
         rng = np.random.default_rng(seed(spec.index, 0))
-        amp = 0.2 if mesh.etype == "hex" or mesh.etype == "tri" else 0.12
+        amp = 0.2 if mesh.etype in ("hex", "hexs", "tri") else 0.12
         mesh = perturb_and_permute(mesh, rng, h, amp)
     elif variant != "structured":
         raise ValueError(variant)
@@ -194,9 +228,9 @@ def make_state(name: str, mesh: Mesh, prob: Problem, kind: str = "random"):
         st[0, 0] = rng.uniform(0.0, 1.0, N)
     elif name == "c2":
         st[0, 0] = rng.uniform(300.0, 1200.0, N)
-    elif name in ("c3", "c5"):
+    elif name in ("c3", "c5", "q2", "s2"):
         st[0] = rng.uniform(-1e-3, 1e-3, (kh, N))
-    elif name == "c4":
+    elif name in ("c4", "q2ns"):
         U, H = 0.45, 0.41
         y, z = x[1], x[2]
         uw = 16 * U * (H - y) * (H - z) * y * z / H ** 4  # P:1050 inflow profile

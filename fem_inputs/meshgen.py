@@ -5,6 +5,9 @@ Conventions (readings L7/L8/L19):
   * tri  (P1): (0,0),(1,0),(0,1) reference vertices, counter-clockwise.
   * tet  (P1): v0..v3; (P2): + edge nodes (0,1),(1,2),(0,2),(0,3),(1,3),(2,3)  [VTK quadratic tetra].
   * hex  (Q1): (---),(+--),(++-),(-+-),(--+),(+-+),(+++),(-++)  [VTK hexahedron].
+  * hex (Q2, 27 nodes) / hexs (serendipity, 20 nodes), reading L28: the 8 corners as Q1, the 12 edge
+    midpoints of VTK's quadratic hexahedron (0,1),(1,2),(2,3),(3,0),(4,5),(5,6),(6,7),(7,4),(0,4),(1,5),
+    (2,6),(3,7), then (27 only) the face centres in facet order x-,x+,y-,y+,z-,z+ and the centre.
   * Facet k: tri edge (k, k+1 mod 3); tet face opposite vertex k; hex faces
     x-(0,4,7,3) x+(1,2,6,5) y-(0,1,5,4) y+(3,7,6,2) z-(0,3,2,1) z+(4,5,6,7).
 The facet vertex lists below are only used to *select* boundary facets lying on a plane; the
@@ -22,6 +25,24 @@ FACET_VERTS = {
     "tet": [(1, 2, 3), (0, 2, 3), (0, 1, 3), (0, 1, 2)],
     "hex": [(0, 4, 7, 3), (1, 2, 6, 5), (0, 1, 5, 4), (3, 7, 6, 2), (0, 3, 2, 1), (4, 5, 6, 7)],
 }
+FACET_VERTS["hexs"] = FACET_VERTS["hex"]
+
+_HEX_CORNERS = [(-1, -1, -1), (1, -1, -1), (1, 1, -1), (-1, 1, -1), (-1, -1, 1), (1, -1, 1), (1, 1, 1), (-1, 1, 1)]
+_HEX_EDGES = [(0, 1), (1, 2), (2, 3), (3, 0), (4, 5), (5, 6), (6, 7), (7, 4), (0, 4), (1, 5), (2, 6), (3, 7)]
+
+
+def quad_cube_ref_nodes(n_loc: int):
+    """Reference coordinates r_a ∈ {-1,0,1}³ of the 20/27 nodes of a quadratic cube (reading L28)."""
+    r = [tuple(c) for c in _HEX_CORNERS]
+    for a, b in _HEX_EDGES:
+        r.append(tuple((_HEX_CORNERS[a][d] + _HEX_CORNERS[b][d]) // 2 for d in range(3)))
+    if n_loc == 27:
+        for f in range(6):
+            c = [0, 0, 0]
+            c[f // 2] = 1 if f & 1 else -1
+            r.append(tuple(c))
+        r.append((0, 0, 0))
+    return np.array(r[:n_loc], dtype=np.int64)
 
 
 @dataclass
@@ -83,6 +104,27 @@ def hex_box(nx: int, ny: int, nz: int, lx=1.0, ly=1.0, lz=1.0) -> Mesh:
 
 
 _P2_EDGES = [(0, 1), (1, 2), (0, 2), (0, 3), (1, 3), (2, 3)]
+
+
+def hex_box_quadratic(nx: int, ny: int, nz: int, lx=1.0, ly=1.0, lz=1.0, serendipity: bool = False) -> Mesh:
+    """Structured box of quadratic cubes (NEXT-2): 27-node Lagrange ("hex", order 2) or 20-node serendipity
+    ("hexs", order 2).  Nodes are the points of the doubled lattice (id by x fastest) — all of them for the
+    27-node cube; for serendipity only the points with at most one odd lattice coordinate (vertices and edge
+    midpoints), renumbered in the same order."""
+    mx, my, mz = 2 * nx, 2 * ny, 2 * nz
+    I, J, K = np.meshgrid(np.arange(mx + 1), np.arange(my + 1), np.arange(mz + 1), indexing="ij")
+    I, J, K = (a.transpose(2, 1, 0).ravel() for a in (I, J, K))
+    keep = ((I & 1) + (J & 1) + (K & 1) <= 1) if serendipity else np.ones(I.shape, bool)
+    new_id = np.full(I.shape, -1, dtype=np.int64)
+    new_id[keep] = np.arange(int(keep.sum()))
+    coords = np.stack([I[keep] * (lx / mx), J[keep] * (ly / my), K[keep] * (lz / mz)])
+    ei, ej, ek = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    ei, ej, ek = (a.transpose(2, 1, 0).ravel() for a in (ei, ej, ek))
+    ref = quad_cube_ref_nodes(20 if serendipity else 27)
+    lid = lambda a, b, c: a + (mx + 1) * (b + (my + 1) * c)  # noqa: E731
+    conn = np.stack([new_id[lid(2 * ei + 1 + r[0], 2 * ej + 1 + r[1], 2 * ek + 1 + r[2])] for r in ref])
+    assert (conn >= 0).all()
+    return Mesh(3, "hexs" if serendipity else "hex", 2, _soa(coords, np.float64), _soa(conn, np.int32))
 
 
 def tet_box(nx: int, ny: int, nz: int, lx=1.0, ly=1.0, lz=1.0, order: int = 1) -> Mesh:
@@ -164,6 +206,7 @@ def perturb_and_permute(mesh: Mesh, rng: np.random.Generator, h, amp: float = 0.
     h = np.broadcast_to(np.asarray(h, dtype=np.float64), (mesh.dim,))
     bnd = _boundary_node_mask(mesh, lo, hi)
     nv = 3 if mesh.etype == "tri" else (4 if mesh.etype == "tet" else 8)
+    quad_cube = mesh.etype in ("hex", "hexs") and mesh.order == 2
     vert_ids = np.unique(mesh.conn[:nv])
     interior = vert_ids[~bnd[vert_ids]]
     jit = rng.uniform(-1.0, 1.0, size=(mesh.dim, interior.size)) * (amp * h)[:, None]
@@ -172,6 +215,11 @@ def perturb_and_permute(mesh: Mesh, rng: np.random.Generator, h, amp: float = 0.
         for k, (a, b) in enumerate(_P2_EDGES):
             mid = mesh.conn[4 + k]
             coords[:, mid] = 0.5 * (coords[:, mesh.conn[a]] + coords[:, mesh.conn[b]])
+    if quad_cube:  # non-vertex nodes on the trilinear map of the (perturbed) corners
+        ref = quad_cube_ref_nodes(mesh.n_loc)
+        for a in range(8, mesh.n_loc):
+            w = [np.prod([(1 + ref[a][d] * _HEX_CORNERS[c][d]) / 2 for d in range(3)]) for c in range(8)]
+            coords[:, mesh.conn[a]] = sum(w[c] * coords[:, mesh.conn[c]] for c in range(8))
     N, E = mesh.n_nodes, mesh.n_elems
     new_of_old = rng.permutation(N)
     c2 = np.empty_like(coords)

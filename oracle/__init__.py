@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fem_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-ETYPE = {"tri": 1, "tet": 2, "hex": 4}
+ETYPE = {"tri": 1, "tet": 2, "hex": 4, "hexs": 5}
 PHYSICS = {"thermal": 1, "elasticity": 2, "ns": 3}
 FORM = {
     "THERMAL_DOMAIN": 0, "THERMAL_CONV_RAD": 1, "THERMAL_FIX": 2,
@@ -95,7 +95,7 @@ def lib():
         L.or_get.argtypes = [P] + [P] * 9
         L.or_get_slot.argtypes = [P, P, P]
         L.or_free.argtypes = [P]
-        L.or_qp_data.argtypes = [C.POINTER(_Problem), I64, P, I64, P, I64, C.c_int, P, P, P, P, P]
+        L.or_qp_data.argtypes = [C.POINTER(_Problem), I64, P, I64, P, I64, C.c_int, P, P, P, P, P, P]
         _lib = L
         del PI32, PF64
     return _lib
@@ -167,19 +167,20 @@ def assemble(mesh, prob, state, row_mask=None, matrix=True, residual=True, slot=
 
 
 def qp_data(mesh, prob, e: int, facet: int = -1):
-    """Quadrature-point probe: dict(x, w, n, N, G) for element e (volume rule, or facet `facet`)."""
+    """Quadrature-point probe: dict(x, w, n, N, G, H) for element e (volume rule, or facet `facet`);
+    H = physical second derivatives of the shape functions [nq][n_loc][3][3]."""
     L = lib()
     P = make_problem(prob, mesh.dim)
     coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
     conn = np.ascontiguousarray(mesh.conn, dtype=np.int32)
     nl = mesh.n_loc
     x, w, n = np.zeros((64, 3)), np.zeros(64), np.zeros((64, 3))
-    N, G = np.zeros((64, nl)), np.zeros((64, nl, 3))
+    N, G, H = np.zeros((64, nl)), np.zeros((64, nl, 3)), np.zeros((64, nl, 3, 3))
     nq = L.or_qp_data(C.byref(P), mesh.n_nodes, _ptr(coords), mesh.n_elems, _ptr(conn), e, facet,
-                      _ptr(x), _ptr(w), _ptr(n), _ptr(N), _ptr(G))
+                      _ptr(x), _ptr(w), _ptr(n), _ptr(N), _ptr(G), _ptr(H))
     if nq < 0:
         raise ValueError(f"oracle qp_data error {nq}")
-    return dict(x=x[:nq], w=w[:nq], n=n[:nq], N=N[:nq], G=G[:nq])
+    return dict(x=x[:nq], w=w[:nq], n=n[:nq], N=N[:nq], G=G[:nq], H=H[:nq])
 
 
 def to_dense(out, n_cols):

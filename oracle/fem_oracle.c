@@ -25,7 +25,7 @@
 #define M_PI 3.14159265358979323846
 #endif
 
-#define MAXN 10 /* nodes per element (P2 tet)                     */
+#define MAXN 27 /* nodes per element (Q2 hex)                     */
 #define MAXK 4  /* basic-variable components κ̂ (NS: u1,u2,u3,p) */
 #define MAXQ 64
 
@@ -35,6 +35,8 @@ static int n_loc_of(int etype, int order) {
   if (etype == OR_TET && order == 1) return 4;
   if (etype == OR_TET && order == 2) return 10;
   if (etype == OR_HEX && order == 1) return 8;
+  if (etype == OR_HEX && order == 2) return 27; /* Lagrange cube of order 2      */
+  if (etype == OR_HEXS && order == 2) return 20; /* serendipity cube of order 2   */
   return -1;
 }
 static int n_vert_of(int etype) { return etype == OR_TRI ? 3 : (etype == OR_TET ? 4 : 8); }
@@ -43,9 +45,84 @@ static const double HEX_SIGN[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1
                                       {-1, -1, 1},  {1, -1, 1},  {1, 1, 1},  {-1, 1, 1}};
 static const int TET_EDGE[6][2] = {{0, 1}, {1, 2}, {0, 2}, {0, 3}, {1, 3}, {2, 3}};
 
-/* Lagrange shape functions N_a(ξ) and reference gradients ∂N_a/∂ξ_j (φ^h = Σ N_α φ_α). */
-static void shape(int etype, int order, const double* xi, double* N, double dN[][3]) {
+/* Quadratic cubes (NEXT-2; reading L28): reference coordinates r_a ∈ {-1,0,1}³ of the nodes — corners in
+ * VTK order (L7), the 12 edge midpoints of VTK's quadratic hexahedron ((0,1),(1,2),(2,3),(3,0),(4,5),(5,6),
+ * (6,7),(7,4),(0,4),(1,5),(2,6),(3,7)), then (27-node only) the face centres in facet order x-,x+,y-,y+,z-,z+
+ * (L8) and the centre. */
+static const int HEX_EDGE[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                    {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+static void quad_cube_node(int a, double* r) {
+  if (a < 8) { for (int d = 0; d < 3; d++) r[d] = HEX_SIGN[a][d]; return; }
+  if (a < 20) {
+    for (int d = 0; d < 3; d++) r[d] = 0.5 * (HEX_SIGN[HEX_EDGE[a - 8][0]][d] + HEX_SIGN[HEX_EDGE[a - 8][1]][d]);
+    return;
+  }
+  r[0] = r[1] = r[2] = 0.0;
+  if (a < 26) r[(a - 20) / 2] = ((a - 20) & 1) ? 1.0 : -1.0;
+}
+/* 1D quadratic Lagrange factor on the nodes {-1, 0, 1}: value, first and second derivative at t */
+static void lag1d(double r, double t, double* v, double* d1, double* d2) {
+  if (r < -0.5) { *v = 0.5 * t * (t - 1.0); *d1 = t - 0.5; *d2 = 1.0; }
+  else if (r > 0.5) { *v = 0.5 * t * (t + 1.0); *d1 = t + 0.5; *d2 = 1.0; }
+  else { *v = 1.0 - t * t; *d1 = -2.0 * t; *d2 = -2.0; }
+}
+/* N = c Π_d f_d(ξ_d) with per-axis factors (value v, derivatives d1, d2): gradient and Hessian. */
+static void product3(double c, const double* v, const double* d1, const double* d2, double* N, double* g,
+                     double h[3][3]) {
+  *N = c * v[0] * v[1] * v[2];
+  for (int d = 0; d < 3; d++) {
+    int e1 = (d + 1) % 3, e2 = (d + 2) % 3;
+    g[d] = c * d1[d] * v[e1] * v[e2];
+    if (h) h[d][d] = c * d2[d] * v[e1] * v[e2];
+  }
+  if (h)
+    for (int d = 0; d < 3; d++)
+      for (int e = 0; e < 3; e++)
+        if (d != e) h[d][e] = c * d1[d] * d1[e] * v[3 - d - e];
+}
+/* 27-node Lagrange cube: tensor product of the 1D quadratics. */
+static void shape_q2(const double* xi, double* N, double dN[][3], double (*d2N)[3][3]) {
+  for (int a = 0; a < 27; a++) {
+    double r[3], v[3], d1[3], d2[3];
+    quad_cube_node(a, r);
+    for (int d = 0; d < 3; d++) lag1d(r[d], xi[d], &v[d], &d1[d], &d2[d]);
+    product3(1.0, v, d1, d2, &N[a], dN[a], d2N ? d2N[a] : NULL);
+  }
+}
+/* 20-node serendipity cube, the textbook basis:
+ *   corner (r ∈ {±1}³): N = 1/8 Π_d (1 + r_d ξ_d) · (Σ_d r_d ξ_d − 2);
+ *   edge midpoint with r_m = 0: N = 1/4 (1 − ξ_m²) Π_{d≠m} (1 + r_d ξ_d). */
+static void shape_s2(const double* xi, double* N, double dN[][3], double (*d2N)[3][3]) {
+  for (int a = 0; a < 20; a++) {
+    double r[3], v[3], d1[3], d2[3];
+    quad_cube_node(a, r);
+    if (a < 8) {
+      double f, fg[3], fh[3][3];
+      for (int d = 0; d < 3; d++) { v[d] = 1.0 + r[d] * xi[d]; d1[d] = r[d]; d2[d] = 0.0; }
+      product3(0.125, v, d1, d2, &f, fg, fh);
+      double sv = r[0] * xi[0] + r[1] * xi[1] + r[2] * xi[2] - 2.0;
+      N[a] = f * sv;
+      for (int d = 0; d < 3; d++) dN[a][d] = fg[d] * sv + f * r[d];
+      if (d2N)
+        for (int d = 0; d < 3; d++)
+          for (int e = 0; e < 3; e++) d2N[a][d][e] = fh[d][e] * sv + fg[d] * r[e] + fg[e] * r[d];
+    } else {
+      for (int d = 0; d < 3; d++) {
+        if (r[d] == 0.0) { v[d] = 1.0 - xi[d] * xi[d]; d1[d] = -2.0 * xi[d]; d2[d] = -2.0; }
+        else { v[d] = 1.0 + r[d] * xi[d]; d1[d] = r[d]; d2[d] = 0.0; }
+      }
+      product3(0.25, v, d1, d2, &N[a], dN[a], d2N ? d2N[a] : NULL);
+    }
+  }
+}
+
+/* Lagrange shape functions N_a(ξ), reference gradients ∂N_a/∂ξ_j and (d2N != NULL) reference second
+ * derivatives ∂²N_a/∂ξ_j∂ξ_l (φ^h = Σ N_α φ_α; the second derivatives feed μ u_i,kk). */
+static void shape(int etype, int order, const double* xi, double* N, double dN[][3], double (*d2N)[3][3]) {
   memset(dN, 0, sizeof(double) * 3 * MAXN);
+  if (d2N) memset(d2N, 0, sizeof(double) * 9 * MAXN);
+  if (etype == OR_HEX && order == 2) { shape_q2(xi, N, dN, d2N); return; }
+  if (etype == OR_HEXS) { shape_s2(xi, N, dN, d2N); return; }
   if (etype == OR_TRI) { /* P1 triangle, vertices (0,0),(1,0),(0,1) */
     N[0] = 1.0 - xi[0] - xi[1]; N[1] = xi[0]; N[2] = xi[1];
     dN[0][0] = -1; dN[0][1] = -1; dN[1][0] = 1; dN[2][1] = 1;
@@ -61,11 +138,17 @@ static void shape(int etype, int order, const double* xi, double* N, double dN[]
     for (int a = 0; a < 4; a++) { /* vertex: L(2L-1) */
       N[a] = L[a] * (2.0 * L[a] - 1.0);
       for (int j = 0; j < 3; j++) dN[a][j] = (4.0 * L[a] - 1.0) * dL[a][j];
+      if (d2N)
+        for (int j = 0; j < 3; j++)
+          for (int l = 0; l < 3; l++) d2N[a][j][l] = 4.0 * dL[a][j] * dL[a][l];
     }
     for (int k = 0; k < 6; k++) { /* edge (p,q): 4 L_p L_q */
       int p = TET_EDGE[k][0], q = TET_EDGE[k][1];
       N[4 + k] = 4.0 * L[p] * L[q];
       for (int j = 0; j < 3; j++) dN[4 + k][j] = 4.0 * (L[p] * dL[q][j] + L[q] * dL[p][j]);
+      if (d2N)
+        for (int j = 0; j < 3; j++)
+          for (int l = 0; l < 3; l++) d2N[4 + k][j][l] = 4.0 * (dL[p][j] * dL[q][l] + dL[q][j] * dL[p][l]);
     }
     return;
   }
@@ -77,13 +160,17 @@ static void shape(int etype, int order, const double* xi, double* N, double dN[]
     dN[a][0] = 0.125 * HEX_SIGN[a][0] * f[1] * f[2];
     dN[a][1] = 0.125 * HEX_SIGN[a][1] * f[0] * f[2];
     dN[a][2] = 0.125 * HEX_SIGN[a][2] * f[0] * f[1];
+    if (d2N)
+      for (int d = 0; d < 3; d++)
+        for (int e = 0; e < 3; e++)
+          if (d != e) d2N[a][d][e] = 0.125 * HEX_SIGN[a][d] * HEX_SIGN[a][e] * f[3 - d - e];
   }
 }
 
 /* Reference vertex coordinates (for facet parameterisations). */
 static void ref_vertex(int etype, int v, double* out) {
   out[0] = out[1] = out[2] = 0.0;
-  if (etype == OR_HEX) { for (int d = 0; d < 3; d++) out[d] = HEX_SIGN[v][d]; return; }
+  if (etype == OR_HEX || etype == OR_HEXS) { for (int d = 0; d < 3; d++) out[d] = HEX_SIGN[v][d]; return; }
   if (v >= 1) out[v - 1] = 1.0; /* simplex: v0 = origin, v_k = e_k */
 }
 
@@ -202,6 +289,8 @@ static int facet_rule(int etype, int q, int facet, double pts[][3], double* w, d
 typedef struct {
   double x[3], w, n[3];
   double N[MAXN], G[MAXN][3];
+  double H[MAXN][3][3]; /* ∂²N_a/∂x_i∂x_j (physical)                 */
+  double lap[MAXN];     /* Σ_k ∂²N_a/∂x_k∂x_k: feeds μ u_i,kk */
 } qpt;
 
 typedef struct {
@@ -225,8 +314,8 @@ static double det3(double J[3][3]) {
 static int eval_point(const ctx* c, int64_t e, const double* xi, double wref, const double* t1,
                       const double* t2, int is_facet, qpt* q) {
   int dim = c->dim, nl = c->nloc;
-  double dN[MAXN][3], X[MAXN][3];
-  shape(c->P->etype, c->P->order, xi, q->N, dN);
+  double dN[MAXN][3], X[MAXN][3], d2N[MAXN][3][3];
+  shape(c->P->etype, c->P->order, xi, q->N, dN, d2N);
   for (int a = 0; a < nl; a++) {
     int64_t node = c->conn[(int64_t)a * c->E + e];
     for (int d = 0; d < dim; d++) X[a][d] = c->coords[(int64_t)d * c->N + node];
@@ -264,6 +353,31 @@ static int eval_point(const ctx* c, int64_t e, const double* xi, double wref, co
     if (i < dim)
       for (int a = 0; a < nl; a++) q->x[i] += q->N[a] * X[a][i];
   }
+  /* Second derivatives (chain rule twice): ∂²N/∂ξ_j∂ξ_l = Σ_im H_im J_ij J_ml + Σ_i G_i ∂²x_i/∂ξ_j∂ξ_l, so
+   * H = J^{-T} (∂²N/∂ξ² − Σ_i G_i ∂²x_i/∂ξ²) J^{-1}, with ∂²x_i/∂ξ_j∂ξ_l = Σ_a x_{a,i} ∂²N_a/∂ξ_j∂ξ_l. */
+  double Xh[3][3][3] = {{{0}}}; /* Xh[i][j][l] = ∂²x_i/∂ξ_j∂ξ_l */
+  for (int i = 0; i < dim; i++)
+    for (int j = 0; j < dim; j++)
+      for (int l = 0; l < dim; l++)
+        for (int a = 0; a < nl; a++) Xh[i][j][l] += X[a][i] * d2N[a][j][l];
+  for (int a = 0; a < nl; a++) {
+    double A[3][3] = {{0}}; /* reference-space Hessian minus the geometric term */
+    for (int j = 0; j < dim; j++)
+      for (int l = 0; l < dim; l++) {
+        A[j][l] = d2N[a][j][l];
+        for (int i = 0; i < dim; i++) A[j][l] -= q->G[a][i] * Xh[i][j][l];
+      }
+    q->lap[a] = 0.0;
+    for (int i = 0; i < 3; i++)
+      for (int m = 0; m < 3; m++) {
+        double h = 0.0;
+        if (i < dim && m < dim)
+          for (int j = 0; j < dim; j++)
+            for (int l = 0; l < dim; l++) h += inv[j][i] * A[j][l] * inv[l][m];
+        q->H[a][i][m] = h;
+      }
+    for (int i = 0; i < dim; i++) q->lap[a] += q->H[a][i][i];
+  }
   if (!is_facet) { q->w = wref * fabs(det); return 0; }
   double T1[3] = {0, 0, 0}, T2[3] = {0, 0, 0}, dA;
   for (int i = 0; i < dim; i++)
@@ -293,6 +407,7 @@ static int eval_point(const ctx* c, int64_t e, const double* xi, double wref, co
 typedef struct {
   double v[3][MAXK]; /* v[ν][κ]: value of ∂_t^ν φ̃^κ  */
   double g[MAXK][3]; /* g[κ][i]: ∂φ̃^κ/∂x_i (level 0) */
+  double l[MAXK];    /* l[κ]: Σ_k ∂²φ̃^κ/∂x_k² (level 0), the u_i,kk of Rm */
 } fld;
 
 static void eval_fields(const ctx* c, int64_t e, const qpt* q, const double* state, fld* f) {
@@ -303,8 +418,10 @@ static void eval_fields(const ctx* c, int64_t e, const qpt* q, const double* sta
     for (int nu = 0; nu < levels && nu < 3; nu++)
       for (int k = 0; k < c->kh; k++)
         f->v[nu][k] += q->N[b] * state[((int64_t)nu * c->kh + k) * c->N + node];
-    for (int k = 0; k < c->kh; k++)
+    for (int k = 0; k < c->kh; k++) {
       for (int i = 0; i < c->dim; i++) f->g[k][i] += q->G[b][i] * state[(int64_t)k * c->N + node];
+      f->l[k] += q->lap[b] * state[(int64_t)k * c->N + node];
+    }
   }
 }
 
@@ -380,11 +497,12 @@ static double res(const ctx* c, const or_term* t, const qpt* q, const fld* f, in
   double rho = p[0], mu = p[1];
   const double* u = f->v[0];
   double pr = f->v[0][dim];
-  double Rc = 0.0, Rm[3] = {0, 0, 0}; /* P:979; μ u_i,kk = 0 for P1 (L10) */
+  double Rc = 0.0, Rm[3] = {0, 0, 0}; /* Rm_i = ρ u_k u_i,k + p_,i − μ u_i,kk (0 for P1, L10) */
   for (int k = 0; k < dim; k++) Rc += f->g[k][k];
   for (int i = 0; i < dim; i++) {
     Rm[i] = f->g[dim][i];
     for (int k = 0; k < dim; k++) Rm[i] += rho * u[k] * f->g[i][k];
+    Rm[i] -= mu * f->l[i];
   }
   double Gn = 0.0, un = 0.0;
   for (int j = 0; j < dim; j++) { Gn += q->G[a][j] * q->n[j]; un += u[j] * q->n[j]; }
@@ -482,6 +600,8 @@ static double dres(const ctx* c, const or_term* t, const qpt* q, const fld* f, c
       Rm[i] += rho * u[k] * f->g[i][k];
       dRm[i] += rho * (du[k] * f->g[i][k] + u[k] * df->g[i][k]);
     }
+    Rm[i] -= mu * f->l[i];   /* − μ u_i,kk */
+    dRm[i] -= mu * df->l[i];
   }
   double Gn = 0.0, un = 0.0, dun = 0.0;
   for (int j = 0; j < dim; j++) {
@@ -656,6 +776,7 @@ static void add_point(or_system* s, const ctx* c, const or_term* t, int64_t e, c
       memset(&df, 0, sizeof(df));
       for (int nu = 0; nu < levels && nu < 3; nu++) df.v[nu][kl] = time_factor(c->P, nu) * q->N[b];
       for (int i = 0; i < dim; i++) df.g[kl][i] = time_factor(c->P, 0) * q->G[b][i];
+      df.l[kl] = time_factor(c->P, 0) * q->lap[b];
       for (int a = 0; a < nl; a++) {
         if (li[a] < 0) continue;
         int64_t deg = s->rowptr_s[li[a] + 1] - s->rowptr_s[li[a]];
@@ -680,7 +801,7 @@ or_system* or_assemble(const or_problem* P, int64_t n_nodes, const double* coord
   ctx c = {P, n_nodes, n_elems, coords, conn, n_loc_of(P->etype, P->order), P->dim, 0};
   c.kh = P->physics == OR_THERMAL ? 1 : (P->physics == OR_ELASTICITY ? P->dim : P->dim + 1);
   s->N = n_nodes; s->E = n_elems; s->nloc = c.nloc; s->kh = c.kh;
-  if (c.nloc < 0 || (P->etype == OR_TRI) != (P->dim == 2) || (P->physics == OR_NS && P->order != 1)) {
+  if (c.nloc < 0 || (P->etype == OR_TRI) != (P->dim == 2)) {
     s->status = -2;
     return s;
   }
@@ -781,7 +902,7 @@ void or_free(or_system* s) {
 
 int or_qp_data(const or_problem* P, int64_t n_nodes, const double* coords, int64_t n_elems,
                const int32_t* conn, int64_t e, int facet, double* x, double* w, double* n,
-               double* N, double* G) {
+               double* N, double* G, double* H) {
   ctx c = {P, n_nodes, n_elems, coords, conn, n_loc_of(P->etype, P->order), P->dim, 1};
   if (c.nloc < 0) return -2;
   double pts[MAXQ][3], wr[MAXQ], t1[MAXQ][3], t2[MAXQ][3];
@@ -798,6 +919,9 @@ int or_qp_data(const or_problem* P, int64_t n_nodes, const double* coords, int64
     for (int a = 0; a < c.nloc; a++) {
       N[g * c.nloc + a] = q.N[a];
       for (int d = 0; d < 3; d++) G[(g * c.nloc + a) * 3 + d] = q.G[a][d];
+      if (H)
+        for (int d = 0; d < 3; d++)
+          for (int d2 = 0; d2 < 3; d2++) H[((g * c.nloc + a) * 3 + d) * 3 + d2] = q.H[a][d][d2];
     }
   }
   return nq;

@@ -16,7 +16,7 @@
 extern "C" {
 #endif
 
-enum { OR_TRI = 1, OR_TET = 2, OR_HEX = 4 };
+enum { OR_TRI = 1, OR_TET = 2, OR_HEX = 4, OR_HEXS = 5 }; /* HEXS: 20-node serendipity cube (order 2) */
 enum { OR_THERMAL = 1, OR_ELASTICITY = 2, OR_NS = 3 };
 enum {
   OR_THERMAL_DOMAIN = 0, OR_THERMAL_CONV_RAD = 1, OR_THERMAL_FIX = 2,
@@ -57,11 +57,12 @@ void or_get_slot(const or_system* s, const int32_t* conn, int32_t* slot_s);
 void or_free(or_system* s);
 
 /* Probe: quadrature-point data of element e (facet < 0: volume rule; else facet `facet`).
- * Outputs (capacity 64 points): x [nq][3], w [nq], n [nq][3], N [nq][n_loc], G [nq][n_loc][3].
+ * Outputs (capacity 64 points): x [nq][3], w [nq], n [nq][3], N [nq][n_loc], G [nq][n_loc][3],
+ * H [nq][n_loc][3][3] (physical second derivatives ∂²N_a/∂x_i∂x_j; may be NULL).
  * Returns nq, or a negative error. */
 int or_qp_data(const or_problem* prob, int64_t n_nodes, const double* coords, int64_t n_elems,
                const int32_t* conn, int64_t e, int facet, double* x, double* w, double* n,
-               double* N, double* G);
+               double* N, double* G, double* H);
 
 #ifdef __cplusplus
 }
