@@ -42,12 +42,17 @@ extern "C" {
 /* ---- element types (reading L7: VTK node orders; reference simplex / [-1,1]^3 cube) */
 #define FEM_TRI 1 /* order 1: 3 nodes                                   */
 #define FEM_TET 2 /* order 1: 4 nodes; order 2: 10 nodes (VTK edge order) */
-#define FEM_HEX 4 /* order 1: 8 nodes                                   */
+#define FEM_HEX 4 /* order 1: 8 nodes; order 2: 27-node Lagrange cube (NEXT-2)          */
+#define FEM_HEX_SERENDIPITY 5 /* order 2: 20-node serendipity cube (NEXT-2)            */
+/* Quadratic cube node order (reading L28): 8 corners as the Q1 hex, the 12 edge midpoints of VTK's
+ * quadratic hexahedron (0,1),(1,2),(2,3),(3,0),(4,5),(5,6),(6,7),(7,4),(0,4),(1,5),(2,6),(3,7), then for
+ * the 27-node cube the 6 face centres in facet order x-,x+,y-,y+,z-,z+ and the centre.  Quadrature:
+ * quad_order 2 or 3 Gauss-Legendre points per axis.  Facets are integrated over all element nodes (L18). */
 
 /* ---- physics (κ̂ = number of scalar basic variables, reading L2/L3) */
 #define FEM_THERMAL 1    /* κ̂ = 1: T  */
 #define FEM_ELASTICITY 2 /* κ̂ = dim: d_1..d_dim  */
-#define FEM_NS 3         /* κ̂ = dim+1: u_1..u_dim, p (3D, P1 only)  */
+#define FEM_NS 3         /* κ̂ = dim+1: u_1..u_dim, p (3D; Rm carries −μ u_i,kk) */
 
 /* ---- weak forms: the paper's named groups; params[] layout per form */
 #define FEM_WF_THERMAL_DOMAIN 0   /* -C(T,T_t) - k(T_,i,T_,i) + (T,s)    P:821,832 params {C, k, s, source_kind(0 const, 1 s·Π sin(π x_d))} */

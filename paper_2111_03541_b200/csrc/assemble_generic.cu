@@ -23,6 +23,8 @@ int launch_generic(const AsmArgs& A, bool facet) {
   if (et == ET_HEX && o == 1) return gen_dispatch_hex(m->kh, A.quad_order, P, A.stream, facet);
   if (et == ET_TET && o == 1) return gen_dispatch_tet1(m->kh, A.quad_order, P, A.stream, facet);
   if (et == ET_TET && o == 2) return gen_dispatch_tet2(m->kh, A.quad_order, P, A.stream, facet);
+  if (et == ET_HEX && o == 2) return gen_dispatch_hex2(m->kh, A.quad_order, P, A.stream, facet);
+  if (et == ET_HEXS && o == 2) return gen_dispatch_hexs2(m->kh, A.quad_order, P, A.stream, facet);
   set_error("unsupported element type/order");
   return FEM_E_UNSUPPORTED;
 }

@@ -175,6 +175,58 @@ __global__ void __launch_bounds__(128) k_generic(const GenParams P) {
       } else {
         q.w = wref * det;
       }
+      if constexpr (qp_has_lap<DIM, NL, KH>() && !FACET) {  // (boundary forms do not use Rm)
+        // L_a = tr H_a with H = J^{-T} (∂²N/∂ξ² − Σ_i G_i ∂²x_i/∂ξ²) J^{-1} (chain rule twice); first the
+        // geometry's second derivatives Xh_i = Σ_a x_ai ∂²N_a/∂ξ², then per node (Hessians recomputed)
+        double Xh[DIM][DIM][DIM];
+#pragma unroll
+        for (int i = 0; i < DIM; i++)
+#pragma unroll
+          for (int j = 0; j < DIM; j++)
+#pragma unroll
+            for (int l = 0; l < DIM; l++) Xh[i][j][l] = 0.0;
+        for (int a = 0; a < NL; a++) {
+          double h[3][3];
+          EL::node_hess(a, xi, h);
+#pragma unroll
+          for (int i = 0; i < DIM; i++)
+#pragma unroll
+            for (int j = 0; j < DIM; j++)
+#pragma unroll
+              for (int l = 0; l < DIM; l++) Xh[i][j][l] += X[a][i] * h[j][l];
+        }
+        double JJ[DIM][DIM];  // J^{-1} J^{-T}: tr(J^{-T} A J^{-1}) = Σ_jl A_jl (J^{-1} J^{-T})_lj
+#pragma unroll
+        for (int l = 0; l < DIM; l++)
+#pragma unroll
+          for (int j = 0; j < DIM; j++) {
+            double t = 0.0;
+#pragma unroll
+            for (int i = 0; i < DIM; i++) t += Ji[l][i] * Ji[j][i];
+            JJ[l][j] = t;
+          }
+        for (int a = 0; a < NL; a++) {
+          double h[3][3];
+          EL::node_hess(a, xi, h);
+          double L = 0.0;
+#pragma unroll
+          for (int j = 0; j < DIM; j++)
+#pragma unroll
+            for (int l = 0; l < DIM; l++) {
+              double A = h[j][l];
+#pragma unroll
+              for (int i = 0; i < DIM; i++) A -= q.G[a][i] * Xh[i][j][l];
+              L += A * JJ[l][j];
+            }
+          q.L[a] = L;
+        }
+#pragma unroll
+        for (int k = 0; k < KH; k++) {
+          double t = 0.0;
+          for (int a = 0; a < NL; a++) t += q.L[a] * P.state[(int64_t)k * P.N + nd[a]];
+          q.lu[k] = t;
+        }
+      }
       // fields
 #pragma unroll
       for (int k = 0; k < KH; k++) {
@@ -257,7 +309,10 @@ inline int run(const GenParams& P, cudaStream_t s) {
 
 template <int ET, int ORD, int KH, bool FACET>
 inline int run_q(int q, const GenParams& P, cudaStream_t s) {
-  if constexpr (ET == ET_HEX) {
+  if constexpr ((ET == ET_HEX || ET == ET_HEXS) && ORD == 2) {  // quadratic cubes: 2 or 3 points per axis
+    if (q == 2) return run<ET, ORD, KH, 2, FACET>(P, s);
+    if (q == 3) return run<ET, ORD, KH, 3, FACET>(P, s);
+  } else if constexpr (ET == ET_HEX) {
     if (q == 1) return run<ET, ORD, KH, 1, FACET>(P, s);
     if (q == 2) return run<ET, ORD, KH, 2, FACET>(P, s);
     if (q == 3) return run<ET, ORD, KH, 3, FACET>(P, s);
@@ -273,5 +328,7 @@ int gen_dispatch_tri(int kh, int q, const GenParams& P, cudaStream_t s, bool fac
 int gen_dispatch_hex(int kh, int q, const GenParams& P, cudaStream_t s, bool facet);
 int gen_dispatch_tet1(int kh, int q, const GenParams& P, cudaStream_t s, bool facet);
 int gen_dispatch_tet2(int kh, int q, const GenParams& P, cudaStream_t s, bool facet);
+int gen_dispatch_hex2(int kh, int q, const GenParams& P, cudaStream_t s, bool facet);
+int gen_dispatch_hexs2(int kh, int q, const GenParams& P, cudaStream_t s, bool facet);
 
 }  // namespace fem

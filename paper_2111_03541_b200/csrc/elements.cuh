@@ -13,7 +13,7 @@
 
 namespace fem {
 
-enum { ET_TRI = 1, ET_TET = 2, ET_HEX = 4 };
+enum { ET_TRI = 1, ET_TET = 2, ET_HEX = 4, ET_HEXS = 5 };  // ET_HEXS: 20-node serendipity cube
 
 // ---------------------------------------------------------------- 1D Gauss-Legendre on [-1,1]
 __host__ __device__ inline void gauss_legendre(int n, int i, double& x, double& w) {
@@ -105,6 +105,11 @@ struct TetRules {
 
 template <> struct Elem<ET_TET, 1> : TetRules {
   static constexpr int DIM = 3, NL = 4, NV = 4, NF = 4;
+  static constexpr bool CURVED2 = false;  // reference second derivatives vanish
+  __host__ __device__ static void node_hess(int, const double*, double (*h)[3]) {
+    for (int j = 0; j < 3; j++)
+      for (int l = 0; l < 3; l++) h[j][l] = 0.0;
+  }
   __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
     double L[4];
     tet_bary(xi, L);
@@ -117,6 +122,15 @@ template <> struct Elem<ET_TET, 1> : TetRules {
 
 template <> struct Elem<ET_TET, 2> : TetRules {
   static constexpr int DIM = 3, NL = 10, NV = 4, NF = 4;
+  static constexpr bool CURVED2 = true;
+  // ∂²N_a/∂ξ_j∂ξ_l: vertex L(2L-1) -> 4 ∂L_j ∂L_l; edge 4 L_p L_q -> 4(∂L_p,j ∂L_q,l + ∂L_q,j ∂L_p,l)
+  __host__ __device__ static void node_hess(int a, const double*, double (*h)[3]) {
+    const int EP[6] = {0, 1, 0, 0, 1, 2}, EQ[6] = {1, 2, 2, 3, 3, 3};
+    for (int j = 0; j < 3; j++)
+      for (int l = 0; l < 3; l++)
+        h[j][l] = a < 4 ? 4.0 * dbary(a, j) * dbary(a, l)
+                        : 4.0 * (dbary(EP[a - 4], j) * dbary(EQ[a - 4], l) + dbary(EQ[a - 4], j) * dbary(EP[a - 4], l));
+  }
   __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
     const int EP[6] = {0, 1, 0, 0, 1, 2}, EQ[6] = {1, 2, 2, 3, 3, 3};
     double L[4];
@@ -143,6 +157,14 @@ __host__ __device__ inline double hex_sign(int a, int d) {
 
 template <> struct Elem<ET_HEX, 1> {
   static constexpr int DIM = 3, NL = 8, NV = 8, NF = 6;
+  static constexpr bool CURVED2 = true;  // trilinear: mixed second derivatives
+  __host__ __device__ static void node_hess(int a, const double* xi, double (*h)[3]) {
+    double f[3];
+    for (int d = 0; d < 3; d++) f[d] = 0.5 * (1.0 + hex_sign(a, d) * xi[d]);
+    for (int j = 0; j < 3; j++)
+      for (int l = 0; l < 3; l++)
+        h[j][l] = (j == l) ? 0.0 : 0.25 * hex_sign(a, j) * hex_sign(a, l) * f[3 - j - l];
+  }
   __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
     for (int a = 0; a < 8; a++) {
       const double fx = 0.5 * (1.0 + hex_sign(a, 0) * xi[0]);
@@ -177,6 +199,120 @@ template <> struct Elem<ET_HEX, 1> {
     w = ws * wt;
     mref[0] = mref[1] = mref[2] = 0.0;
     mref[axis] = side;
+  }
+};
+
+// ---------------------------------------------------------------- quadratic cubes (NEXT-2, reading L28)
+// Node a sits at ξ = q_a ∈ {-1,0,1}³: corners in VTK order, the 12 edge midpoints of VTK's quadratic
+// hexahedron, then (27-node) the face centres in facet order x-,x+,y-,y+,z-,z+ and the centre.
+// Encoded as base-3 digits (q+1) per axis, x fastest: corners 0,2,8,6,18,20,26,24 etc.
+__host__ __device__ inline int qc_code(int a) {
+  const int T[27] = {0, 2, 8, 6, 18, 20, 26, 24,                   // corners (---),(+--),(++-),(-+-),(--+)...
+                     1, 5, 7, 3, 19, 23, 25, 21, 9, 11, 17, 15,    // edges (0,1),(1,2),(2,3),(3,0),(4,5)...(3,7)
+                     12, 14, 10, 16, 4, 22, 13};                   // faces x-,x+,y-,y+,z-,z+; centre
+  return T[a];
+}
+__host__ __device__ inline int qc_coord(int a, int d) {  // q_a,d ∈ {-1,0,1}
+  int c = qc_code(a);
+  for (int k = 0; k < d; k++) c /= 3;
+  return c % 3 - 1;
+}
+// 1D quadratic Lagrange basis on {-1,0,1}: (value, first, second derivative) of node q at t
+__host__ __device__ inline void lq1(int q, double t, double& v, double& d1, double& d2) {
+  if (q == 0) { v = (1.0 - t) * (1.0 + t); d1 = -2.0 * t; d2 = -2.0; }
+  else { v = 0.5 * t * (t + q); d1 = t + 0.5 * q; d2 = 1.0; }
+}
+
+// 27-node Lagrange cube: N_a = Π_d ℓ_{q_a,d}(ξ_d)
+template <> struct Elem<ET_HEX, 2> {
+  static constexpr int DIM = 3, NL = 27, NV = 8, NF = 6;
+  static constexpr bool CURVED2 = true;
+  __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
+    double v[3][3], d1[3][3], d2[3][3];  // [axis][node coordinate + 1]
+    for (int d = 0; d < 3; d++)
+      for (int q = -1; q <= 1; q++) lq1(q, xi[d], v[d][q + 1], d1[d][q + 1], d2[d][q + 1]);
+    for (int a = 0; a < 27; a++) {
+      const int i = qc_coord(a, 0) + 1, j = qc_coord(a, 1) + 1, k = qc_coord(a, 2) + 1;
+      N[a] = v[0][i] * v[1][j] * v[2][k];
+      dN[a][0] = d1[0][i] * v[1][j] * v[2][k];
+      dN[a][1] = v[0][i] * d1[1][j] * v[2][k];
+      dN[a][2] = v[0][i] * v[1][j] * d1[2][k];
+    }
+  }
+  __host__ __device__ static void node_hess(int a, const double* xi, double (*h)[3]) {
+    double v[3], d1[3], d2[3];
+    for (int d = 0; d < 3; d++) lq1(qc_coord(a, d), xi[d], v[d], d1[d], d2[d]);
+    for (int j = 0; j < 3; j++)
+      for (int l = 0; l < 3; l++) {
+        const int m = 3 - j - l;
+        h[j][l] = (j == l) ? d2[j] * v[(j + 1) % 3] * v[(j + 2) % 3] : d1[j] * d1[l] * v[m];
+      }
+  }
+  __host__ __device__ static constexpr int vol_nq(int q) { return q * q * q; }
+  __host__ __device__ static void vol_qp(int q, int i, double* xi, double& w) { Elem<ET_HEX, 1>::vol_qp(q, i, xi, w); }
+  __host__ __device__ static constexpr int fac_nq(int q) { return q * q; }
+  __host__ __device__ static void fac_qp(int q, int f, int i, double* xi, double& w, double* mref) {
+    Elem<ET_HEX, 1>::fac_qp(q, f, i, xi, w, mref);
+  }
+};
+
+// 20-node serendipity cube: corners N = ⅛ Π(1 + q_d ξ_d)(q·ξ - 2); edge midpoints (q_m = 0)
+// N = ¼ (1 - ξ_m²) Π_{d≠m}(1 + q_d ξ_d).  Value / gradient / Hessian of one node from its three factors.
+struct SerendipityNode {
+  double N, g[3], h[3][3];
+  __host__ __device__ SerendipityNode(int a, const double* xi) {
+    double f[3], f1[3], f2[3];
+    int q[3], zero = -1;
+    for (int d = 0; d < 3; d++) {
+      q[d] = qc_coord(a, d);
+      if (q[d] == 0) { zero = d; f[d] = 1.0 - xi[d] * xi[d]; f1[d] = -2.0 * xi[d]; f2[d] = -2.0; }
+      else { f[d] = 1.0 + q[d] * xi[d]; f1[d] = q[d]; f2[d] = 0.0; }
+    }
+    const double c = zero < 0 ? 0.125 : 0.25;
+    double P = c * f[0] * f[1] * f[2], Pg[3], Ph[3][3];
+    for (int j = 0; j < 3; j++)
+      for (int l = 0; l < 3; l++) {
+        const int m = 3 - j - l;
+        Ph[j][l] = (j == l) ? c * f2[j] * f[(j + 1) % 3] * f[(j + 2) % 3] : c * f1[j] * f1[l] * f[m];
+      }
+    for (int j = 0; j < 3; j++) Pg[j] = c * f1[j] * f[(j + 1) % 3] * f[(j + 2) % 3];
+    if (zero >= 0) {  // edge midpoint: the product itself
+      N = P;
+      for (int j = 0; j < 3; j++) {
+        g[j] = Pg[j];
+        for (int l = 0; l < 3; l++) h[j][l] = Ph[j][l];
+      }
+    } else {  // corner: product × (q·ξ - 2)
+      const double s = q[0] * xi[0] + q[1] * xi[1] + q[2] * xi[2] - 2.0;
+      N = P * s;
+      for (int j = 0; j < 3; j++) {
+        g[j] = Pg[j] * s + P * q[j];
+        for (int l = 0; l < 3; l++) h[j][l] = Ph[j][l] * s + Pg[j] * q[l] + Pg[l] * q[j];
+      }
+    }
+  }
+};
+
+template <> struct Elem<ET_HEXS, 2> {
+  static constexpr int DIM = 3, NL = 20, NV = 8, NF = 6;
+  static constexpr bool CURVED2 = true;
+  __host__ __device__ static void shape(const double* xi, double* N, double (*dN)[3]) {
+    for (int a = 0; a < 20; a++) {
+      const SerendipityNode s(a, xi);
+      N[a] = s.N;
+      for (int d = 0; d < 3; d++) dN[a][d] = s.g[d];
+    }
+  }
+  __host__ __device__ static void node_hess(int a, const double* xi, double (*h)[3]) {
+    const SerendipityNode s(a, xi);
+    for (int j = 0; j < 3; j++)
+      for (int l = 0; l < 3; l++) h[j][l] = s.h[j][l];
+  }
+  __host__ __device__ static constexpr int vol_nq(int q) { return q * q * q; }
+  __host__ __device__ static void vol_qp(int q, int i, double* xi, double& w) { Elem<ET_HEX, 1>::vol_qp(q, i, xi, w); }
+  __host__ __device__ static constexpr int fac_nq(int q) { return q * q; }
+  __host__ __device__ static void fac_qp(int q, int f, int i, double* xi, double& w, double* mref) {
+    Elem<ET_HEX, 1>::fac_qp(q, f, i, xi, w, mref);
   }
 };
 

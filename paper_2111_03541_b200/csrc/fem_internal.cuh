@@ -156,6 +156,8 @@ struct fem_pattern_s {
   int32_t* slot = nullptr;      // device [n_loc²][E]
   int64_t* rowptr = nullptr;    // device [n_rows+1]
   int32_t* colidx = nullptr;    // device [nnz]
+  int tiles_rc = 0;             // != 0: no tile schedule for this mesh (tiled calls return it)
+  std::string tiles_msg;
 };
 
 namespace fem {

@@ -21,6 +21,8 @@ static int n_loc_of(int et, int order) {
   if (et == FEM_TET && order == 1) return 4;
   if (et == FEM_TET && order == 2) return 10;
   if (et == FEM_HEX && order == 1) return 8;
+  if (et == FEM_HEX && order == 2) return 27;              // Lagrange cube of order 2 (NEXT-2)
+  if (et == FEM_HEX_SERENDIPITY && order == 2) return 20;  // serendipity cube of order 2
   return -1;
 }
 
@@ -132,7 +134,7 @@ int fem_mesh_create(const fem_problem* prob, int dim, int64_t n_nodes, const dou
   }
   const int nl = n_loc_of(prob->etype, prob->order);
   const int kh = kappa_hat_of(prob->physics, dim);
-  if (nl < 0 || kh < 0 || (prob->etype == FEM_TRI) != (dim == 2) || (prob->physics == FEM_NS && (dim != 3 || prob->order != 1))) {
+  if (nl < 0 || kh < 0 || (prob->etype == FEM_TRI) != (dim == 2) || (prob->physics == FEM_NS && dim != 3)) {
     set_error("fem_mesh_create: unsupported element/order/physics/dimension combination");
     return FEM_E_UNSUPPORTED;
   }
@@ -267,8 +269,23 @@ int fem_pattern_build(fem_mesh_t m, void* stream, fem_pattern_t* out, int64_t* n
   fem_pattern_s* p = new fem_pattern_s();
   p->mesh = m;
   int rc = pattern_build(m, (cudaStream_t)stream, p);
-  if (rc == 0) rc = tiles_build(m, p, (cudaStream_t)stream);
   if (rc != 0) { fem_pattern_destroy(p); return rc; }
+  // The node-tile schedule of FEM_SCATTER_TILED is built with the pattern (one-time).  When the mesh
+  // does not fit it (an element type without a tile kernel, a row wider than the 8-bit local offsets, a
+  // row larger than the shared accumulator) the pattern is still valid for the atomic and coloured scatters;
+  // tiled calls then fail with FEM_E_UNSUPPORTED and this reason.
+  if (m->order == 2 && (m->etype == FEM_HEX || m->etype == FEM_HEX_SERENDIPITY)) {
+    p->tiles_rc = FEM_E_UNSUPPORTED;
+    p->tiles_msg = "tiled scatter: no tile kernel for quadratic cubes (use FEM_SCATTER_COLOURED or _ATOMIC)";
+  } else {
+    const int trc = tiles_build(m, p, (cudaStream_t)stream);
+    if (trc == FEM_E_OOM || trc == FEM_E_CUDA) { fem_pattern_destroy(p); return trc; }
+    if (trc != 0) {
+      p->tiles_rc = trc;
+      p->tiles_msg = fem_last_error();
+      tiles_free(p->tiles);
+    }
+  }
   m->last_n_tiles = p->tiles.n_tiles;
   if (n_rows) *n_rows = p->n_rows;
   if (nnz) *nnz = p->nnz;
@@ -346,6 +363,7 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
   if (scatter == FEM_SCATTER_TILED) {
     if (accumulate) { set_error("tiled scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
     if (!p) { set_error("tiled scatter needs the pattern"); return FEM_E_INVALID_ARG; }
+    if (p->tiles_rc) { set_error(p->tiles_msg); return p->tiles_rc; }
     // NS on P1 tets: the generic boundary terms (1% of the visits) would stall the whole tile
     // behind a facet phase run by a few warps (22% of c4); they run instead as the deterministic coloured
     // facet pass over the rows the tile kernel has written (FEM_NS_FACET_PHASE=1 keeps the in-tile phase)

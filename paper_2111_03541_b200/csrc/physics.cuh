@@ -7,14 +7,26 @@
 // factor f_ν of the operand (Eq. gen_alpha).
 //   Thermal     P:821-823 (code P:832-835)   κ̂ = 1
 //   Elasticity  P:900-906 (code P:913-923)   κ̂ = dim, λ = Eν/((1+ν)(1-2ν)), μ = E/(2(1+ν))
-//   NS + SUPG   P:979-992 (code P:998-1025)  κ̂ = dim+1 (u_1..u_dim, p); u_i,kk = 0 on P1 (L10)
+//   NS + SUPG   P:979-992 (code P:998-1025)  κ̂ = dim+1 (u_1..u_dim, p); Rm carries −μ u_i,kk, which
+//               vanishes on P1 (L10) and is carried by the QP's Laplacian tables on every other element
 #pragma once
 #include "../../include/libfem.h"
 
 namespace fem {
 
+// NS records on elements whose shape functions have non-zero second derivatives carry the physical
+// Laplacian of every shape function L_a = Σ_k ∂²N_a/∂x_k² and of every operand, lu_κ = Σ_b L_b φ̃^κ_b
+// (for μ u_i,kk in Rm_i).  P1 simplices (NL = DIM + 1) have none.
 template <int DIM, int NL, int KH>
-struct QP {
+constexpr bool qp_has_lap() { return KH == DIM + 1 && NL > DIM + 1; }
+template <int NL, int KH, bool LAP> struct QPLap {};
+template <int NL, int KH> struct QPLap<NL, KH, true> {
+  double L[NL];
+  double lu[KH];
+};
+
+template <int DIM, int NL, int KH>
+struct QP : QPLap<NL, KH, qp_has_lap<DIM, NL, KH>()> {
   double w;           // physical weight ŵ|det J| or ŵ·dA (reading L1)
   double x[DIM];      // physical point
   double n[DIM];      // outward unit normal (facets only)
@@ -105,6 +117,7 @@ __device__ __forceinline__ double form_res(const FormArgs& F, const QP<DIM, NL, 
         Rm_i += rho * q.u[0][k] * q.gu[i][k];
         Aa += q.G[a][k] * q.u[0][k];
       }
+      if constexpr (qp_has_lap<DIM, NL, KH>()) Rm_i -= mu * q.lu[i];  // − μ u_i,kk
       if (!is_p) {
         double r = -q.G[a][i] * pr + tc * q.G[a][i] * Rc + tm * rho * Aa * Rm_i;
 #pragma unroll
@@ -117,6 +130,7 @@ __device__ __forceinline__ double form_res(const FormArgs& F, const QP<DIM, NL, 
         double Rm = q.gu[DIM][ii];
 #pragma unroll
         for (int k = 0; k < DIM; k++) Rm += rho * q.u[0][k] * q.gu[ii][k];
+        if constexpr (qp_has_lap<DIM, NL, KH>()) Rm -= mu * q.lu[ii];
         r += tm * q.G[a][ii] * Rm;
       }
       return r;
@@ -203,8 +217,13 @@ __device__ __forceinline__ double form_tan(const FormArgs& F, const QP<DIM, NL, 
 #pragma unroll
         for (int k = 0; k < DIM; k++) Rm_i += rho * q.u[0][k] * q.gu[i][k];
         const double dim_ = (i == m) ? 1.0 : 0.0;
+        double dlap = 0.0;  // ∂(−μ u_i,kk)/∂φ_(b,m) = −μ δ_im L_b
+        if constexpr (qp_has_lap<DIM, NL, KH>()) {
+          Rm_i -= mu * q.lu[i];
+          dlap = -mu * dim_ * q.L[b];
+        }
         v = -rho * Nb * (dim_ * Aa + q.u[0][i] * q.G[a][m]) + mu * dim_ * GaGb +
-            tm * rho * Nb * q.G[a][m] * Rm_i + tm * rho * rho * Aa * (Nb * q.gu[i][m] + dim_ * Bb) +
+            tm * rho * Nb * q.G[a][m] * Rm_i + tm * rho * Aa * (rho * (Nb * q.gu[i][m] + dim_ * Bb) + dlap) +
             tc * q.G[a][i] * q.G[b][m];
       } else if (!row_p && col_p) {
         v = -q.G[a][i] * Nb + tm * rho * Aa * q.G[b][i];
@@ -213,6 +232,7 @@ __device__ __forceinline__ double form_tan(const FormArgs& F, const QP<DIM, NL, 
 #pragma unroll
         for (int ii = 0; ii < DIM; ii++) s += q.G[a][ii] * q.gu[ii][m];
         v = Na * q.G[b][m] + tm * rho * (Nb * s + q.G[a][m] * Bb);
+        if constexpr (qp_has_lap<DIM, NL, KH>()) v -= tm * mu * q.G[a][m] * q.L[b];
       } else {
         v = tm * GaGb;
       }

@@ -15,10 +15,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FEM_LIB_PATH") or os.path.join(_HERE, "libfem.so")  # override: dev A/B builds
 
-FEM_TRI, FEM_TET, FEM_HEX = 1, 2, 4
+FEM_TRI, FEM_TET, FEM_HEX, FEM_HEX_SERENDIPITY = 1, 2, 4, 5
 FEM_THERMAL, FEM_ELASTICITY, FEM_NS = 1, 2, 3
 SCATTER = {"atomic": 0, "coloured": 1, "tiled": 2}
-ETYPE = {"tri": FEM_TRI, "tet": FEM_TET, "hex": FEM_HEX}
+ETYPE = {"tri": FEM_TRI, "tet": FEM_TET, "hex": FEM_HEX, "hexs": FEM_HEX_SERENDIPITY}
 PHYSICS = {"thermal": FEM_THERMAL, "elasticity": FEM_ELASTICITY, "ns": FEM_NS}
 FORM = {
     "THERMAL_DOMAIN": 0, "THERMAL_CONV_RAD": 1, "THERMAL_FIX": 2,
