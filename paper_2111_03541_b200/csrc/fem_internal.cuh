@@ -61,13 +61,20 @@ struct TileSchedule {
   int64_t* rec_off = nullptr;    // device [n_tiles+1] byte offsets
   int64_t rec_max = 0, rec_bytes_total = 0;
   int max_turns = 0;              // most visits of one tile touching one owned point (ordered kernels need <= 255)
+  // z-sweep schedule (hex meshes on a lattice, sweep.cu): records are the steps of sequences; a CTA walks
+  // one sequence (a column chunk) step by step, carrying accumulator rows in a ring of two node planes.
+  // Row tables of a step record are indexed by ring position; zrow/wrow list the rows to zero at the
+  // step's start and to write at its end.  Plain node tiles are sequences of one record.
+  bool sweep = false;
+  int64_t n_seq = 0;
+  int64_t* seq_off = nullptr;     // device [n_seq+1]: records of sequence q are [seq_off[q], seq_off[q+1])
 };
 
 // Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by
 // 16-byte aligned sections (see rec_layout).  Built on the host at pattern time (loc on the device).
 struct RecLayout {
   int o_tnode, o_tdeg, o_toff, o_trps, o_hnode, o_run, o_velem, o_vhal, o_vown, o_vloc, o_vseq, o_fcnt, o_fdv, o_ffac,
-      o_fseg, size;
+      o_fseg, o_zrow, o_wrow, o_vsw, o_vfm, o_vfst, size;
 };
 // header[6] = number of boundary sets nb, header[7] = facet visits nf; facet visit i of set k
 // (fcnt[k] <= i < fcnt[k+1]) is facet ffac[i] of the tile's domain visit fdv[i].
@@ -77,7 +84,7 @@ struct RecLayout {
 // segment starts; the facets of one segment belong to distinct elements of one colour (node-disjoint),
 // so a deterministic kernel may run a segment's facets concurrently with plain adds.
 __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, int nruns, int nb = 0, int nf = 0,
-                                                int ns = 0) {
+                                                int ns = 0, int nzr = 0, int nwr = 0, int sweep = 0) {
   RecLayout L;
   int o = 48;
   auto al = [](int x) { return (x + 15) & ~15; };
@@ -96,6 +103,13 @@ __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, in
   L.o_fdv = o;   o = al(o + 2 * nf);
   L.o_ffac = o;  o = al(o + nf);
   L.o_fseg = o;  o = al(o + 4 * (nb + 1) + 4 * (ns + 1));
+  L.o_zrow = o;  o = al(o + 2 * nzr);
+  L.o_wrow = o;  o = al(o + 2 * nwr);
+  // sweep records (header[11] = 1): per (visit, node) uint16 turn | first-touch << 14 | last-touch << 15,
+  // per visit the 32-bit boundary-face mask (6 bits per set) and the 64-bit first-contribution mask (a, b)
+  L.o_vsw = o;   o = al(o + (sweep ? 2 * nv * NL : 0));
+  L.o_vfm = o;   o = al(o + (sweep ? 4 * nv : 0));
+  L.o_vfst = o;  o = al(o + (sweep ? 8 * nv : 0));
   L.size = o;
   return L;
 }
@@ -106,8 +120,9 @@ __host__ __device__ inline RecLayout rec_layout(int NL, int T, int H, int nv, in
 __host__ __device__ inline int acc_row_stride(int KH, int d, int64_t nnz_s) {
   return KH == 1 ? d : KH * d + ((KH * (d + (int)(nnz_s & 1))) & 1);
 }
+// header[9] / [10] = number of zrow / wrow entries (sweep steps; 0 for plain tiles)
 __host__ __device__ inline RecLayout rec_layout_hdr(int NL, const int32_t* h) {
-  return rec_layout(NL, h[0], h[1], h[2], h[3], h[6], h[7], h[8]);
+  return rec_layout(NL, h[0], h[1], h[2], h[3], h[6], h[7], h[8], h[9], h[10], h[11]);
 }
 
 }  // namespace fem
@@ -179,6 +194,8 @@ struct AsmArgs {
 };
 
 int launch_generic(const AsmArgs& A, bool facet);
+// z-sweep schedule for Q1-hex elasticity on lattice meshes (sweep.cu); FEM_E_UNSUPPORTED: not applicable
+int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s);
 int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_problem* prob,
                  const double* state, double* values, double* rhs, cudaStream_t stream);
 int pattern_build(fem_mesh_s* m, cudaStream_t stream, fem_pattern_s* p);

@@ -545,7 +545,7 @@ __device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t*
 // Offsets (bytes from the dynamic shared-memory base) of the current tile's arrays: kept in shared
 // memory so every visit addresses them with LDS and without rematerialising the record layout.
 struct TileOffs {
-  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc, vseq, turn;
+  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc, vseq, turn, tnode, trps;
   int H, T;
 };
 // Per-lane constants of the fragment layout: B fragments of the geometry GEMM (6), ∇̂N_a at points c
@@ -665,7 +665,12 @@ __device__ __forceinline__ void hex_el_facets(const TiledParams& P, uint32_t fm,
 // the residual fused into the scatter (f0 = 1), system with the stress-GEMM residual (f0 != 1).
 enum { HX_MAT = 0, HX_RES = 1, HX_SYS_FUSED = 2, HX_SYS = 3 };
 
-template <bool DET, int MODE, bool ORDERED = DET>
+// SW (sweep records, sweep.cu): the turn of each (visit, node) comes from the 16-bit vseq with the row's
+// first-touch (bit 14) and last-touch (bit 15) flags; bit 7 of the local column offset marks the first
+// contribution to a 3x3 block of the row's current life (stored, not added: no zeroing pass); the visit
+// that makes the last touch of a row writes the completed row to HBM before passing the turn on (the
+// ring slot's next occupant starts with the next turn), so no step needs a block-wide epilogue.
+template <bool DET, int MODE, bool ORDERED = DET, bool SW = false>
 __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOffs& to, const HexCoef& H,
                                               const double* __restrict__ lt, double* sc, int v,
                                               unsigned char* sm, const uint32_t* vfm) {
@@ -724,7 +729,8 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       const int li = own[r];
       if (c == 0 && li >= 0) {
         volatile int* tp = reinterpret_cast<volatile int*>(sm + to.turn) + li;
-        const int t = (sm + to.vseq)[v * 8 + r];
+        const int t = SW ? (int)(reinterpret_cast<const uint16_t*>(sm + to.vseq)[v * 8 + r] & 0x3fff)
+                         : (int)(sm + to.vseq)[v * 8 + r];
         while (*tp != t) __nanosleep(64);
         *tp = t + 1;
       }
@@ -866,19 +872,27 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   }
   int* turn = reinterpret_cast<int*>(sm + to.turn);
   int my_turn = 0;
+  unsigned sw_flags = 0;  // SW: bit 14 first touch of the row's life, bit 15 last touch
   if constexpr (ORDERED) {  // wait for this visit's turn on the owned row it writes (record order)
     if (li >= 0) {
-      my_turn = (sm + to.vseq)[v * 8 + a];
+      if constexpr (SW) {
+        const unsigned w = reinterpret_cast<const uint16_t*>(sm + to.vseq)[v * 8 + a];
+        my_turn = (int)(w & 0x3fffu);
+        sw_flags = w;
+      } else {
+        my_turn = (sm + to.vseq)[v * 8 + a];
+      }
       while (ld_acquire_cta(turn + li) != my_turn)  // acquire: the previous holder's row writes are visible
         if (P.spin_ns) __nanosleep(P.spin_ns);
     }
   }
+  const bool row_first = SW && (sw_flags & (1u << 14));
   auto write_res = [&]() {  // GEMM residual: lane (a, c < 2) holds r_(a, 2c), r_(a, 2c + 1)
     if (has_rhs && !fuse && c < 2 && li >= 0) {
       double* racc = reinterpret_cast<double*>(sm + to.racc) + li + 2 * c * to.T;
       if constexpr (DET) {
-        racc[0] += (c == 0 ? fres[0] : fres[2]) - res[0];
-        if (c == 0) racc[to.T] += fres[1] - res[1];
+        racc[0] = (row_first ? 0.0 : racc[0]) + ((c == 0 ? fres[0] : fres[2]) - res[0]);
+        if (c == 0) racc[to.T] = (row_first ? 0.0 : racc[to.T]) + (fres[1] - res[1]);
       } else {
         atomicAdd(racc, (c == 0 ? fres[0] : fres[2]) - res[0]);
         if (c == 0) atomicAdd(racc + to.T, fres[1] - res[1]);
@@ -893,13 +907,15 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
       const uint8_t* lc = sm + to.vloc + v * 64 + a * 8 + 2 * c;
 #pragma unroll
       for (int t = 0; t < 2; t++) {
-        double* rowb = base + lc[t];
+        const unsigned lct = lc[t];
+        double* rowb = base + (SW ? (lct & 0x7fu) : lct);
         if constexpr (DET) {  // independent read-modify-writes: loads first (d may alias for the compiler)
+          const bool first = SW && (lct & 0x80u);  // first contribution to this block: store
 #pragma unroll
           for (int i = 0; i < 3; i++) {
             double old[3];
 #pragma unroll
-            for (int m = 0; m < 3; m++) old[m] = rowb[i * sr + m * d];
+            for (int m = 0; m < 3; m++) old[m] = first ? 0.0 : rowb[i * sr + m * d];
 #pragma unroll
             for (int m = 0; m < 3; m++) rowb[i * sr + m * d] = old[m] + Kv[t][i * 3 + m];
           }
@@ -913,7 +929,7 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
           double* racc = reinterpret_cast<double*>(sm + to.racc) + li;
 #pragma unroll
           for (int i = 0; i < 3; i++) {
-            if constexpr (DET) racc[i * to.T] += res[i] + fres[i];
+            if constexpr (DET) racc[i * to.T] = (row_first ? 0.0 : racc[i * to.T]) + (res[i] + fres[i]);
             else atomicAdd(racc + i * to.T, res[i] + fres[i]);
           }
         }
@@ -921,6 +937,39 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
     }
   }
   __syncwarp();  // scratch is reused by the next visit; the row's four lanes have written
+  if constexpr (SW) {
+    // the rows this visit completes (last touch of their life) leave to HBM now, written by the whole warp:
+    // 3 segments of 3d doubles each (16-byte phase of the destination = phase in the ring, see
+    // acc_row_stride), then the residual rows
+    unsigned lastm = __ballot_sync(0xffffffffu, c == 0 && li >= 0 && (sw_flags & (1u << 15)));
+    while (lastm) {
+      const int src_lane = __ffs(lastm) - 1;
+      lastm &= lastm - 1;
+      const int rl = own[src_lane >> 2];
+      const int32_t* tn = reinterpret_cast<const int32_t*>(sm + to.tnode);
+      const int64_t* trp = reinterpret_cast<const int64_t*>(sm + to.trps);
+      if constexpr (has_values) {
+        const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[rl], sr = acc_row_stride(3, d, P.nnz_s);
+        const double* src = reinterpret_cast<const double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[rl];
+        const int len = 3 * d;
+#pragma unroll
+        for (int k0 = 0; k0 < 3; k0++) {
+          const double* s0 = src + k0 * sr;
+          double* dst = P.values + (int64_t)k0 * 3 * P.nnz_s + (int64_t)3 * trp[rl];
+          const int head = ((uintptr_t)dst & 15) ? 1 : 0;
+          const int npair = (len - head) >> 1;
+          for (int j = lane; j < npair; j += 32)
+            __stcs(reinterpret_cast<double2*>(dst + head) + j, reinterpret_cast<const double2*>(s0 + head)[j]);
+          if (lane == 0 && head) __stcs(dst, s0[0]);
+          if (lane == 1 && head + 2 * npair < len) __stcs(dst + len - 1, s0[len - 1]);
+        }
+      }
+      if (has_rhs && lane < 3)
+        P.rhs[(int64_t)lane * P.n_own + (tn[rl] - P.own_lo)] =
+            reinterpret_cast<const double*>(sm + to.racc)[rl + lane * to.T];
+    }
+    __syncwarp();  // the row's ring slot may be reused by its next life once the turn passes on
+  }
   if constexpr (ORDERED) {  // hand the row to the next visit in record order: a release store, cumulative
     // over the row's four lanes whose writes this lane has observed through __syncwarp
     if (c == 0 && li >= 0) st_release_cta(turn + li, my_turn + 1);
@@ -1009,7 +1058,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
   }
   mbar_wait(&mbar[0], 0);
   gather_halo(P, RBUF(0), HBUF(0));
-  for (int it = 0; tile < P.n_tiles; it++, tile += gridDim.x) {
+  for (int it = 0; tile < P.n_tiles; it++) {
     const int cur = it & 1, oth = cur ^ 1;
     const int64_t next = tile + gridDim.x;
     if (tid == 0 && next < P.n_tiles) {  // prefetch the next record (its buffer was released last iteration)
@@ -1106,6 +1155,195 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
       rec_facets<ET_HEX, 1, KH, 2, FACET_WARPS, DET>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % FACET_WARPS));
     tile_epilogue<KH>(P, F);
     __syncthreads();
+    tile = next;
+  }
+}
+
+// ---- z-sweep kernel (sweep.cu schedules): 15 consumer warps take the element visits of the steps of
+// this CTA's sequences, in order; warp 15 is the producer: it streams the step records (TMA bulk copy)
+// and their halo points (LDGSTS) into a 3-deep ring, signalled by mbarriers (full: record + halo landed,
+// empty: every consumer warp is done with the step).  Consumers never wait for each other except through
+// the per-row turns of the ordered accumulation (and one named barrier between sequences, which resets
+// the turn counters): rows are zeroed by their first contribution and written by their last toucher.
+constexpr int SW_CONSUMERS = HEX_WARPS - 1;
+constexpr int SW_NBUF = 3;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_constant__ TiledParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [SW_NBUF]
+  uint64_t* empty = full + SW_NBUF;                     // [SW_NBUF]
+  uint64_t* landed = empty + SW_NBUF;                   // [SW_NBUF] record bulk copies
+  __shared__ double lanetab[32 * LANE_TAB];
+  auto rbuf = [&](int b) { return smem + 128 + (size_t)b * P.rec_cap; };
+  auto hbuf = [&](int b) { return reinterpret_cast<double*>(smem + 128 + (size_t)SW_NBUF * P.rec_cap) + (size_t)b * P.hcap; };
+  double* acc = hbuf(SW_NBUF);
+  int* turn = reinterpret_cast<int*>(acc + P.acc_cap);
+  double* scratch = reinterpret_cast<double*>(turn + P.turn_cap);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  HexCoef Hc = {0, 0, 0, 0, 0, 0};
+  for (int f = 0; f < P.n_dom; f++) {
+    const FormArgs& Fm = P.dom[f];
+    Hc.cl += Fm.f0 * Fm.lam; Hc.cm += Fm.f0 * Fm.mu; Hc.sl += Fm.lam; Hc.sm += Fm.mu;
+  }
+  if (warp == 0) {  // per-lane constant table (same for every warp), transposed
+    const GeoFrag GF = geo_frag();
+    double* Lt = lanetab + tid;
+#pragma unroll
+    for (int s2 = 0; s2 < 2; s2++)
+#pragma unroll
+      for (int t = 0; t < 3; t++) Lt[32 * (s2 * 3 + t)] = GF.b[s2][t];
+    double g0[3], g1[3], N0, N1;
+    hex_ref(tid >> 2, tid & 3, g0, N0);
+    hex_ref(tid >> 2, (tid & 3) + 4, g1, N1);
+    for (int i = 0; i < 3; i++) { Lt[32 * (6 + i)] = g0[i]; Lt[32 * (9 + i)] = g1[i]; }
+    double gc[3], gc4[3], Nc, Nc4;
+    hex_ref(tid & 3, tid >> 2, gc, Nc);
+    hex_ref((tid & 3) + 4, tid >> 2, gc4, Nc4);
+    for (int i = 0; i < 3; i++) { Lt[32 * (12 + i)] = gc[i]; Lt[32 * (15 + i)] = gc4[i]; }
+  }
+  if (tid == 0) {
+    for (int b = 0; b < SW_NBUF; b++) {
+      mbar_init(&full[b], 32);             // the producer's 32 lanes (cp.async arrive.noinc)
+      mbar_init(&empty[b], SW_CONSUMERS);  // one arrive per consumer warp
+      mbar_init(&landed[b], 1);
+    }
+    mbar_fence_init();
+  }
+  for (int i = tid; i < P.turn_cap; i += blockDim.x) turn[i] = 0;
+  __syncthreads();
+  int64_t q = blockIdx.x;
+  if (q >= P.n_seq) return;
+  int64_t t = P.seq_off[q];
+  auto next_of = [&](int64_t tt, int64_t& qq) -> int64_t {
+    if (tt + 1 < P.seq_off[qq + 1]) return tt + 1;
+    qq += gridDim.x;
+    return qq < P.n_seq ? P.seq_off[qq] : P.n_tiles;
+  };
+  if (warp == SW_CONSUMERS) {
+    // ---------------- producer
+    for (int64_t k = 0; t < P.n_tiles; k++) {
+      const int b = (int)(k % SW_NBUF);
+      const uint32_t use = (uint32_t)(k / SW_NBUF);
+      if (k >= SW_NBUF) mbar_wait(&empty[b], (use - 1) & 1u);  // all consumers left step k - SW_NBUF
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)(P.rec_off[t + 1] - P.rec_off[t]);
+        mbar_expect_tx(&landed[b], bytes);
+        bulk_g2s(rbuf(b), P.rec + P.rec_off[t], bytes, &landed[b]);
+      }
+      mbar_wait(&landed[b], use & 1u);
+      const uint8_t* rec = rbuf(b);
+      const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+      const int H = hdr[1];
+      const RecLayout L = rec_layout_hdr(8, hdr);
+      const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
+      double* hb = hbuf(b);
+      for (int c = 0; c < P.hcomp; c++) {
+        const double* base = c < 3 ? P.coords + (int64_t)c * P.N : P.state + (int64_t)(c - 3) * P.N;
+        for (int i = lane; i < H; i += 32) cp_async8(hb + c * H + i, base + hn[i]);
+      }
+      cp_async_mbar_arrive_noinc(&full[b]);
+      t = next_of(t, q);
+    }
+    return;
+  }
+  // ---------------- consumers
+  double* wsc = scratch + (size_t)HEX_SCRATCH * warp;
+  for (int64_t k = 0; t < P.n_tiles; k++) {
+    const int b = (int)(k % SW_NBUF);
+    mbar_wait(&full[b], (uint32_t)(k / SW_NBUF) & 1u);
+    mbar_wait(&landed[b], (uint32_t)(k / SW_NBUF) & 1u);  // (already complete) the record's bulk copy is visible
+    const uint8_t* rec = rbuf(b);
+    const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
+    const RecLayout L = rec_layout_hdr(8, hdr);
+    const int nv = hdr[2];
+    const int acc_n = P.values ? hdr[4] : 0;
+    TileOffs to;
+    const uint32_t rb = (uint32_t)(rec - smem);
+    to.vown = rb + L.o_vown; to.vhal = rb + L.o_vhal; to.velem = rb + L.o_velem; to.vloc = rb + L.o_vloc;
+    to.hdat = (uint32_t)(reinterpret_cast<const unsigned char*>(hbuf(b)) - smem);
+    to.tdeg = rb + L.o_tdeg; to.toff = rb + L.o_toff; to.tnode = rb + L.o_tnode; to.trps = rb + L.o_trps;
+    to.acc = (uint32_t)(reinterpret_cast<unsigned char*>(acc) - smem);
+    to.racc = to.acc + 8u * (uint32_t)acc_n;
+    to.vseq = rb + L.o_vsw;
+    to.turn = (uint32_t)(reinterpret_cast<unsigned char*>(turn) - smem);
+    to.H = hdr[1];
+    to.T = hdr[0];
+    const uint32_t* vfm = reinterpret_cast<const uint32_t*>(rec + L.o_vfm);
+    for (int v = warp; v < nv; v += SW_CONSUMERS)
+      hex_visit_el2<true, MODE, true, true>(P, to, Hc, lanetab, wsc, v, smem, vfm);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+    const int64_t qprev = q;
+    t = next_of(t, q);
+    if (q != qprev) {  // sequence boundary: every consumer is done with the old rows; restart the turns
+      asm volatile("bar.sync 1, %0;" ::"r"(SW_CONSUMERS * 32) : "memory");
+      for (int i = tid; i < P.turn_cap; i += SW_CONSUMERS * 32) turn[i] = 0;
+      asm volatile("bar.sync 1, %0;" ::"r"(SW_CONSUMERS * 32) : "memory");
+    }
+  }
+}
+
+static int run_hex_sweep(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
+  P.fac_inline = 1;  // elasticity boundary terms (fix / load) inside the owning element's visit
+  for (int f = 0; f < P.n_fac; f++) {
+    const int fo = P.fac[f].form;
+    if ((fo != FEM_WF_ELAST_FIX_ALL && fo != FEM_WF_ELAST_FIX_D1 && fo != FEM_WF_ELAST_LOAD) || P.fac_set[f] > 4)
+      P.fac_inline = 0;
+  }
+  if (!P.fac_inline) {
+    set_error("hex sweep kernel: boundary terms must be integrated inside the visits (elasticity fix/load forms "
+              "on boundary sets 0..4)");
+    return FEM_E_UNSUPPORTED;
+  }
+  P.seq_off = T.seq_off;
+  P.n_seq = T.n_seq;
+  P.rec = T.rec;
+  P.rec_off = T.rec_off;
+  P.n_tiles = T.n_tiles;
+  P.hcomp = 3 + 3 * (P.nu_hat >= 1 ? 2 : 1);
+  P.rec_cap = (int)((T.rec_max + 15) / 16 * 16);
+  P.hcap = (int)(((T.max_halo * P.hcomp) + 1) / 2 * 2);
+  P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)3 * T.max_tile_nodes);
+  P.acc_cap = (P.acc_cap + 1) / 2 * 2;
+  P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
+  P.spin_ns = 0;
+  const size_t smem = 128 + SW_NBUF * (size_t)P.rec_cap + SW_NBUF * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap +
+                      4 * (size_t)P.turn_cap + 8 * (size_t)HEX_SCRATCH * SW_CONSUMERS;
+  HexCoef Hc = {0, 0, 0, 0, 0, 0};
+  for (int f = 0; f < P.n_dom; f++) {
+    Hc.cl += P.dom[f].f0 * P.dom[f].lam; Hc.cm += P.dom[f].f0 * P.dom[f].mu;
+    Hc.sl += P.dom[f].lam; Hc.sm += P.dom[f].mu;
+  }
+  const int hmode = !P.rhs ? HX_MAT : !P.values ? HX_RES : (Hc.cl == Hc.sl && Hc.cm == Hc.sm) ? HX_SYS_FUSED : HX_SYS;
+  auto launch = [&](auto kern) -> int {
+    cudaFuncAttributes fa;
+    FEM_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+    if (smem + fa.sharedSizeBytes > 227 * 1024) {
+      set_error("hex sweep kernel: shared memory request too large (" + std::to_string(smem) + " B dynamic)");
+      return FEM_E_UNSUPPORTED;
+    }
+    FEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (T.n_tiles <= 0) return 0;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>(T.n_seq, sms);
+    kern<<<(unsigned)grid, HEX_THREADS, smem, s>>>(P);
+    FEM_CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  switch (hmode) {
+    case HX_MAT: return launch(k_hex_sweep<HX_MAT>);
+    case HX_RES: return launch(k_hex_sweep<HX_RES>);
+    case HX_SYS_FUSED: return launch(k_hex_sweep<HX_SYS_FUSED>);
+    default: return launch(k_hex_sweep<HX_SYS>);
   }
 }
 
@@ -1165,6 +1403,13 @@ int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cu
   }
   if (kh != 1 && kh != 3) return 0;
   *handled = true;
+  if (T.sweep) {
+    if (kh != 3 || !det) {
+      set_error("hex sweep schedule: ordered elasticity only");
+      return FEM_E_UNSUPPORTED;
+    }
+    return run_hex_sweep(P, T, s);
+  }
   if (T.rec && !getenv("FEM_NO_RECORDS")) {
     if (det) return kh == 3 ? run_hex_rec<3, true>(P, T, s) : run_hex_rec<1, true>(P, T, s);
     return kh == 3 ? run_hex_rec<3, false>(P, T, s) : run_hex_rec<1, false>(P, T, s);

@@ -90,6 +90,7 @@ static void free_visits(VisitList& V) {
 }
 
 void tiles_free(TileSchedule& T) {
+  cudaFree(T.seq_off);
   cudaFree(T.rec);
   cudaFree(T.rec_off);
   cudaFree(T.halo_off);

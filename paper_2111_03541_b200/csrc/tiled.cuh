@@ -50,6 +50,8 @@ struct TiledParams {
   int spin_ns;   // back-off of a visit waiting for its turn (FEM_SPIN_NS, default 0 = spin)
   int fvmax;     // capacity of the facet visit arrays
   int fac_inline;  // hex elasticity: boundary terms integrated inside the owning element's visit
+  const int64_t* seq_off;  // sweep schedules: record sequences (see TileSchedule)
+  int64_t n_seq;
 };
 
 // Lean point record for elasticity-only domain visits: w, ∇N_a, and w·σ.

@@ -102,3 +102,33 @@ def scatter_rows_into(full_rowptr, full_colidx, rows, rowptr, cols, vals, dst):
         a, b = full_rowptr[g], full_rowptr[g + 1]
         np.testing.assert_array_equal(cols[rowptr[r]:rowptr[r + 1]], full_colidx[a:b])
         dst[a:b] = vals[rowptr[r]:rowptr[r + 1]]
+
+
+def poisoned_system(mesh, problem, own=None):
+    """A FemSystem whose outputs are filled with NaN before every non-accumulating assembly call, so a
+    kernel that skips entries (or a call that silently does nothing) cannot pass on the values an earlier
+    call left in the reused buffers."""
+    from paper_2111_03541_b200 import FemSystem
+
+    class _Poisoned(FemSystem):
+        def _poison(self, matrix, residual, accumulate):
+            self.alloc(matrix, residual)
+            if not accumulate:
+                if matrix:
+                    self.values.fill_(float("nan"))
+                if residual:
+                    self.rhs.fill_(float("nan"))
+
+        def system(self, state, scatter="atomic", accumulate=False):
+            self._poison(True, True, accumulate)
+            return super().system(state, scatter=scatter, accumulate=accumulate)
+
+        def matrix(self, state, scatter="atomic", accumulate=False):
+            self._poison(True, False, accumulate)
+            return super().matrix(state, scatter=scatter, accumulate=accumulate)
+
+        def residual(self, state, scatter="atomic", accumulate=False):
+            self._poison(False, True, accumulate)
+            return super().residual(state, scatter=scatter, accumulate=accumulate)
+
+    return _Poisoned(mesh, problem, own=own)

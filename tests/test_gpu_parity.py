@@ -31,8 +31,8 @@ def _need_gpu():
 
 
 def _gpu_system(m, p, own=None):
-    from paper_2111_03541_b200 import FemSystem
-    return FemSystem(m, p, own=own)
+    from helpers import poisoned_system
+    return poisoned_system(m, p, own=own)
 
 
 def _to_dev(st):
@@ -225,7 +225,7 @@ def test_partitioned_owned_rows_equal_single(name, variant):
         got_v = np.full(len(ora["values"]), np.nan)
         got_r = np.full(len(ora["rhs"]), np.nan)
         for part in parts:
-            S = FemSystem(part.mesh, p, own=part.own)
+            S = _gpu_system(part.mesh, p, own=part.own)
             v, r = S.system(_to_dev(part.local_state(st)), scatter=sc)
             pp = S.export_pattern(slot=False)
             rows, rp, cols, vals = part_csr_to_global(part, pp["rowptr"].cpu().numpy(), pp["colidx"].cpu().numpy(),

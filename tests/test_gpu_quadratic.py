@@ -21,10 +21,10 @@ def _need_gpu():
 
 
 def _check(m, p, st, scatters=("atomic", "coloured")):
-    from paper_2111_03541_b200 import FemSystem
+    from helpers import poisoned_system
     ora = oracle.assemble(m, p, st, slot=True)
     assert ora["status"] == 0
-    S = FemSystem(m, p)
+    S = poisoned_system(m, p)
     pat = S.export_pattern()
     for k in ("rowptr", "colidx", "rowptr_s", "colidx_s", "slot_s"):
         np.testing.assert_array_equal(pat[k].cpu().numpy(), ora[k])
