@@ -883,7 +883,7 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
         my_turn = (sm + to.vseq)[v * 8 + a];
       }
       while (ld_acquire_cta(turn + li) != my_turn)  // acquire: the previous holder's row writes are visible
-        if (P.spin_ns) __nanosleep(P.spin_ns);
+        if (SW || P.spin_ns) __nanosleep(SW ? 32 : P.spin_ns);
     }
   }
   const bool row_first = SW && (sw_flags & (1u << 14));
@@ -938,37 +938,47 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   }
   __syncwarp();  // scratch is reused by the next visit; the row's four lanes have written
   if constexpr (SW) {
-    // the rows this visit completes (last touch of their life) leave to HBM now, written by the whole warp:
-    // 3 segments of 3d doubles each (16-byte phase of the destination = phase in the ring, see
-    // acc_row_stride), then the residual rows
+    // the rows this visit completes (last touch of their life) leave to HBM now: one TMA bulk store per
+    // sub-row (its aligned middle; the 16-byte phase of the ring copy equals the destination's, see
+    // acc_row_stride) plus at most two single doubles, issued by lane 0, which waits until the TMA has read
+    // the ring before the turn passes on (the position's next life starts by storing into it).  Every
+    // accumulator write of every visit is followed by a proxy fence (generic -> async proxy).
+    fence_proxy_async_smem();
+    __syncwarp();
     unsigned lastm = __ballot_sync(0xffffffffu, c == 0 && li >= 0 && (sw_flags & (1u << 15)));
-    while (lastm) {
-      const int src_lane = __ffs(lastm) - 1;
-      lastm &= lastm - 1;
-      const int rl = own[src_lane >> 2];
+    if (lastm) {
       const int32_t* tn = reinterpret_cast<const int32_t*>(sm + to.tnode);
       const int64_t* trp = reinterpret_cast<const int64_t*>(sm + to.trps);
-      if constexpr (has_values) {
-        const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[rl], sr = acc_row_stride(3, d, P.nnz_s);
-        const double* src = reinterpret_cast<const double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[rl];
-        const int len = 3 * d;
-#pragma unroll
-        for (int k0 = 0; k0 < 3; k0++) {
-          const double* s0 = src + k0 * sr;
-          double* dst = P.values + (int64_t)k0 * 3 * P.nnz_s + (int64_t)3 * trp[rl];
-          const int head = ((uintptr_t)dst & 15) ? 1 : 0;
-          const int npair = (len - head) >> 1;
-          for (int j = lane; j < npair; j += 32)
-            __stcs(reinterpret_cast<double2*>(dst + head) + j, reinterpret_cast<const double2*>(s0 + head)[j]);
-          if (lane == 0 && head) __stcs(dst, s0[0]);
-          if (lane == 1 && head + 2 * npair < len) __stcs(dst + len - 1, s0[len - 1]);
+      bool issued = false;
+      while (lastm) {
+        const int src_lane = __ffs(lastm) - 1;
+        lastm &= lastm - 1;
+        const int rl = own[src_lane >> 2];
+        if constexpr (has_values) {
+          if (lane < 3) {  // lane k0 writes sub-row k0
+            const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[rl], sr = acc_row_stride(3, d, P.nnz_s);
+            const double* s0 = reinterpret_cast<const double*>(sm + to.acc) +
+                               reinterpret_cast<const int32_t*>(sm + to.toff)[rl] + lane * sr;
+            double* dst = P.values + (int64_t)lane * 3 * P.nnz_s + (int64_t)3 * trp[rl];
+            const int len = 3 * d;
+            const int head = ((uintptr_t)dst & 15) ? 1 : 0;
+            const int mid = (len - head) & ~1;
+            bulk_s2g(dst + head, s0 + head, 8u * (uint32_t)mid);
+            issued = true;
+            if (head) dst[0] = s0[0];
+            if (head + mid < len) dst[len - 1] = s0[len - 1];
+          }
         }
+        if (has_rhs && lane < 3)
+          P.rhs[(int64_t)lane * P.n_own + (tn[rl] - P.own_lo)] =
+              reinterpret_cast<const double*>(sm + to.racc)[rl + lane * to.T];
       }
-      if (has_rhs && lane < 3)
-        P.rhs[(int64_t)lane * P.n_own + (tn[rl] - P.own_lo)] =
-            reinterpret_cast<const double*>(sm + to.racc)[rl + lane * to.T];
+      if (issued) {
+        bulk_commit();
+        bulk_wait_read_all();
+      }
     }
-    __syncwarp();  // the row's ring slot may be reused by its next life once the turn passes on
+    __syncwarp();  // the ring copies have been read: the positions' next lives may overwrite them
   }
   if constexpr (ORDERED) {  // hand the row to the next visit in record order: a release store, cumulative
     // over the row's four lanes whose writes this lane has observed through __syncwarp
@@ -1231,7 +1241,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
     for (int64_t k = 0; t < P.n_tiles; k++) {
       const int b = (int)(k % SW_NBUF);
       const uint32_t use = (uint32_t)(k / SW_NBUF);
-      if (k >= SW_NBUF) mbar_wait(&empty[b], (use - 1) & 1u);  // all consumers left step k - SW_NBUF
+      if (k >= SW_NBUF) mbar_wait_sleep(&empty[b], (use - 1) & 1u);  // all consumers left step k - SW_NBUF
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)(P.rec_off[t + 1] - P.rec_off[t]);
         mbar_expect_tx(&landed[b], bytes);
@@ -1257,7 +1267,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
   double* wsc = scratch + (size_t)HEX_SCRATCH * warp;
   for (int64_t k = 0; t < P.n_tiles; k++) {
     const int b = (int)(k % SW_NBUF);
-    mbar_wait(&full[b], (uint32_t)(k / SW_NBUF) & 1u);
+    mbar_wait_sleep(&full[b], (uint32_t)(k / SW_NBUF) & 1u);
     mbar_wait(&landed[b], (uint32_t)(k / SW_NBUF) & 1u);  // (already complete) the record's bulk copy is visible
     const uint8_t* rec = rbuf(b);
     const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
