@@ -66,6 +66,7 @@ struct TileSchedule {
   // Row tables of a step record are indexed by ring position; zrow/wrow list the rows to zero at the
   // step's start and to write at its end.  Plain node tiles are sequences of one record.
   bool sweep = false;
+  int sweep_sr = 0;                // ring sub-row stride (81 or 82: fixed 27-column layout, parity of 3·nnz_s)
   int64_t n_seq = 0;
   int64_t* seq_off = nullptr;     // device [n_seq+1]: records of sequence q are [seq_off[q], seq_off[q+1])
 };

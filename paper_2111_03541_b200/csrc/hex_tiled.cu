@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cuda/std/utility>
 #include <string>
+#include <type_traits>
 
 #include "tiled.cuh"
 
@@ -670,7 +671,10 @@ enum { HX_MAT = 0, HX_RES = 1, HX_SYS_FUSED = 2, HX_SYS = 3 };
 // contribution to a 3x3 block of the row's current life (stored, not added: no zeroing pass); the visit
 // that makes the last touch of a row writes the completed row to HBM before passing the turn on (the
 // ring slot's next occupant starts with the next turn), so no step needs a block-wide epilogue.
-template <bool DET, int MODE, bool ORDERED = DET, bool SW = false>
+// SWSR > 0 (sweep rings): every row uses the fixed layout of a 27-column row — entry (i, m, col) at
+// i·SWSR + 27·m + col, SWSR = 81 or 82 (the parity of 3·nnz_s) — so the 18 read-modify-writes of a lane
+// address with immediates; rows with fewer columns (mesh boundary) are compacted when written out.
+template <bool DET, int MODE, bool ORDERED = DET, bool SW = false, int SWSR = 0>
 __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOffs& to, const HexCoef& H,
                                               const double* __restrict__ lt, double* sc, int v,
                                               unsigned char* sm, const uint32_t* vfm) {
@@ -883,7 +887,7 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
         my_turn = (sm + to.vseq)[v * 8 + a];
       }
       while (ld_acquire_cta(turn + li) != my_turn)  // acquire: the previous holder's row writes are visible
-        if (SW || P.spin_ns) __nanosleep(SW ? 32 : P.spin_ns);
+        if (P.spin_ns) __nanosleep(P.spin_ns);
     }
   }
   const bool row_first = SW && (sw_flags & (1u << 14));
@@ -902,7 +906,8 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
   write_res();
   if constexpr (has_values) {
     if (li >= 0) {
-      const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[li], sr = acc_row_stride(3, d, P.nnz_s);
+      const int d = SWSR ? 27 : reinterpret_cast<const int32_t*>(sm + to.tdeg)[li];
+      const int sr = SWSR ? SWSR : acc_row_stride(3, d, P.nnz_s);
       double* base = reinterpret_cast<double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[li];
       const uint8_t* lc = sm + to.vloc + v * 64 + a * 8 + 2 * c;
 #pragma unroll
@@ -955,18 +960,27 @@ __device__ __forceinline__ void hex_visit_el2(const TiledParams& P, const TileOf
         lastm &= lastm - 1;
         const int rl = own[src_lane >> 2];
         if constexpr (has_values) {
-          if (lane < 3) {  // lane k0 writes sub-row k0
-            const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[rl], sr = acc_row_stride(3, d, P.nnz_s);
-            const double* s0 = reinterpret_cast<const double*>(sm + to.acc) +
-                               reinterpret_cast<const int32_t*>(sm + to.toff)[rl] + lane * sr;
-            double* dst = P.values + (int64_t)lane * 3 * P.nnz_s + (int64_t)3 * trp[rl];
-            const int len = 3 * d;
-            const int head = ((uintptr_t)dst & 15) ? 1 : 0;
-            const int mid = (len - head) & ~1;
-            bulk_s2g(dst + head, s0 + head, 8u * (uint32_t)mid);
-            issued = true;
-            if (head) dst[0] = s0[0];
-            if (head + mid < len) dst[len - 1] = s0[len - 1];
+          const int d = reinterpret_cast<const int32_t*>(sm + to.tdeg)[rl];
+          const int sr = SWSR ? SWSR : acc_row_stride(3, d, P.nnz_s);
+          const double* srow = reinterpret_cast<const double*>(sm + to.acc) + reinterpret_cast<const int32_t*>(sm + to.toff)[rl];
+          double* drow = P.values + (int64_t)3 * trp[rl];
+          if (!SWSR || d == 27) {
+            if (lane < 3) {  // lane k0 writes sub-row k0
+              const double* s0 = srow + lane * sr;
+              double* dst = drow + (int64_t)lane * 3 * P.nnz_s;
+              const int len = 3 * d;
+              const int head = ((uintptr_t)dst & 15) ? 1 : 0;
+              const int mid = (len - head) & ~1;
+              bulk_s2g(dst + head, s0 + head, 8u * (uint32_t)mid);
+              issued = true;
+              if (head) dst[0] = s0[0];
+              if (head + mid < len) dst[len - 1] = s0[len - 1];
+            }
+          } else {  // a boundary row (d < 27) in the fixed 27-column layout: compact it while storing
+            for (int idx = lane; idx < 9 * d; idx += 32) {
+              const int k0 = idx / (3 * d), rem = idx - k0 * 3 * d, m = rem / d, col = rem - m * d;
+              drow[(int64_t)k0 * 3 * P.nnz_s + rem] = srow[k0 * sr + 27 * m + col];
+            }
           }
         }
         if (has_rhs && lane < 3)
@@ -1176,7 +1190,6 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_rec(const __grid_constan
 // the per-row turns of the ordered accumulation (and one named barrier between sequences, which resets
 // the turn counters): rows are zeroed by their first contribution and written by their last toucher.
 constexpr int SW_CONSUMERS = HEX_WARPS - 1;
-constexpr int SW_NBUF = 3;
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -1184,9 +1197,10 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int MODE>
+template <int MODE, int SW_NBUF, int SWSR>
 __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  static_assert(3 * SW_NBUF * 8 <= 128, "barriers fit the 128-byte head");
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [SW_NBUF]
   uint64_t* empty = full + SW_NBUF;                     // [SW_NBUF]
   uint64_t* landed = empty + SW_NBUF;                   // [SW_NBUF] record bulk copies
@@ -1265,6 +1279,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
   }
   // ---------------- consumers
   double* wsc = scratch + (size_t)HEX_SCRATCH * warp;
+  int rot = 0;
   for (int64_t k = 0; t < P.n_tiles; k++) {
     const int b = (int)(k % SW_NBUF);
     mbar_wait_sleep(&full[b], (uint32_t)(k / SW_NBUF) & 1u);
@@ -1286,8 +1301,11 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
     to.H = hdr[1];
     to.T = hdr[0];
     const uint32_t* vfm = reinterpret_cast<const uint32_t*>(rec + L.o_vfm);
-    for (int v = warp; v < nv; v += SW_CONSUMERS)
-      hex_visit_el2<true, MODE, true, true>(P, to, Hc, lanetab, wsc, v, smem, vfm);
+    // visits round-robin over the consumers, continuing the rotation of the previous step (49 visits on 15
+    // warps would otherwise always give warps 0-3 the extra visit and let them fall steps behind)
+    for (int v = (warp - rot + SW_CONSUMERS) % SW_CONSUMERS; v < nv; v += SW_CONSUMERS)
+      hex_visit_el2<true, MODE, true, true, SWSR>(P, to, Hc, lanetab, wsc, v, smem, vfm);
+    rot = (rot + nv) % SW_CONSUMERS;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);
     const int64_t qprev = q;
@@ -1323,9 +1341,12 @@ static int run_hex_sweep(TiledParams& P, const TileSchedule& T, cudaStream_t s) 
   P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)3 * T.max_tile_nodes);
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
   P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
-  P.spin_ns = 0;
-  const size_t smem = 128 + SW_NBUF * (size_t)P.rec_cap + SW_NBUF * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap +
-                      4 * (size_t)P.turn_cap + 8 * (size_t)HEX_SCRATCH * SW_CONSUMERS;
+  // a 3-step record/halo ring next to the accumulator ring
+  const size_t fixed = 128 + 8 * (size_t)P.acc_cap + 4 * (size_t)P.turn_cap + 8 * (size_t)HEX_SCRATCH * SW_CONSUMERS;
+  const size_t per_buf = (size_t)P.rec_cap + 8 * (size_t)P.hcap;
+  const int nbuf = 3;
+  const size_t smem = fixed + nbuf * per_buf;
+  P.spin_ns = 32;  // back-off of a visit waiting for its row turn
   HexCoef Hc = {0, 0, 0, 0, 0, 0};
   for (int f = 0; f < P.n_dom; f++) {
     Hc.cl += P.dom[f].f0 * P.dom[f].lam; Hc.cm += P.dom[f].f0 * P.dom[f].mu;
@@ -1349,12 +1370,23 @@ static int run_hex_sweep(TiledParams& P, const TileSchedule& T, cudaStream_t s) 
     FEM_CUDA_TRY(cudaGetLastError());
     return 0;
   };
-  switch (hmode) {
-    case HX_MAT: return launch(k_hex_sweep<HX_MAT>);
-    case HX_RES: return launch(k_hex_sweep<HX_RES>);
-    case HX_SYS_FUSED: return launch(k_hex_sweep<HX_SYS_FUSED>);
-    default: return launch(k_hex_sweep<HX_SYS>);
+  if (nbuf != 3) {
+    set_error("hex sweep kernel: the record ring does not fit (3 steps)");
+    return FEM_E_UNSUPPORTED;
   }
+  auto by_mode = [&](auto srp) -> int {
+    constexpr int SR = decltype(srp)::value;
+    switch (hmode) {
+      case HX_MAT: return launch(k_hex_sweep<HX_MAT, 3, SR>);
+      case HX_RES: return launch(k_hex_sweep<HX_RES, 3, SR>);
+      case HX_SYS_FUSED: return launch(k_hex_sweep<HX_SYS_FUSED, 3, SR>);
+      default: return launch(k_hex_sweep<HX_SYS, 3, SR>);
+    }
+  };
+  if (T.sweep_sr == 81) return by_mode(std::integral_constant<int, 81>());
+  if (T.sweep_sr == 82) return by_mode(std::integral_constant<int, 82>());
+  set_error("hex sweep kernel: unexpected ring row stride");
+  return FEM_E_UNSUPPORTED;
 }
 
 template <int KH, bool DET>

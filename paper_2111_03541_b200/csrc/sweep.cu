@@ -18,6 +18,7 @@
 // fails the check keeps the node-tile schedule.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -127,7 +128,10 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   // every ring position owns a fixed region (even size, one pad double for the 16-byte phase of its row's
   // destination): the lives of a position follow each other in turn order, but lives of DIFFERENT
   // positions are not ordered, so their rows must never share memory
-  const int row_reg = (KH * acc_row_stride(KH, 27, p->nnz_s) + 2) / 2 * 2;
+  // fixed 27-column row layout (hex_visit_el2 SWSR): sub-row stride SR = 3·27 + (1 if nnz_s is even), so that
+  // SR ≡ 3·nnz_s (mod 2) and every sub-row keeps the 16-byte phase of its destination
+  const int SR = 81 + ((p->nnz_s & 1) ? 0 : 1);
+  const int row_reg = (KH * SR + 2) / 2 * 2;
   const int64_t SLOT = (int64_t)PMAX * row_reg;  // doubles per ring plane
   // owned lattice range
   int64_t ob[3][2] = {{1 << 30, -1}, {1 << 30, -1}, {1 << 30, -1}};
@@ -209,7 +213,9 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
         for (int64_t k = 0; k < nsteps; k++) {
           const int64_t l = layers[k];
           std::vector<int32_t>& V = layer_vis[k];
-          // colour runs (the thermal variant sums in colour runs; the ordered variant takes turns)
+          // visit order = turn order, colour-sorted: the visits of one colour share no row, so the visits the
+          // consumer warps take at the same time rarely wait for each other (measured: natural lattice order
+          // 2.6x slower, colours interleaved 1.7x)
           std::stable_sort(V.begin(), V.end(), [&](int32_t a, int32_t b) { return m->h_colour[a] < m->h_colour[b]; });
           std::vector<int32_t> run{0};
           for (size_t v = 1; v < V.size(); v++)
@@ -228,8 +234,8 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
                 r_node[rp] = n;
                 r_rps[rp] = rps[li];
                 r_deg[rp] = (int32_t)(rps[li + 1] - rps[li]);
-                if (KH * acc_row_stride(KH, r_deg[rp], p->nnz_s) + 1 > row_reg) {
-                  set_error("sweep schedule: a row exceeds its ring region");
+                if (r_deg[rp] > 27) {
+                  set_error("sweep schedule: a row has more than 27 scalar columns");
                   return FEM_E_UNSUPPORTED;
                 }
                 int64_t acc = (int64_t)rp * row_reg;                   // even: rp's fixed region
@@ -390,6 +396,7 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   // ---- 4. device copies
   const int64_t n_tiles = (int64_t)roff.size() - 1;
   T.sweep = true;
+  T.sweep_sr = SR;
   T.n_tiles = n_tiles;
   T.n_seq = (int64_t)seq_off.size() - 1;
   T.max_tile_nodes = TR;
