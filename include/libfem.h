@@ -67,11 +67,25 @@ extern "C" {
 #define FEM_WF_NS_BND_OUTFLOW 9   /* BASE + OUTFLOW                      P:991,1015,1024 params {ρ, μ} */
 #define FEM_WF_NS_BND_FIX 10      /* BASE + FIX                          P:992,1017-1018,1025 params {ρ, μ, τ^b} */
 
-/* ---- scatter modes ("(atomic) increment") */
-#define FEM_SCATTER_ATOMIC 0   /* element-parallel, fp64 atomicAdd into values/rhs                  */
-#define FEM_SCATTER_COLOURED 1 /* element colours in fixed order, plain RMW: bit-exact run-to-run   */
-#define FEM_SCATTER_TILED 2    /* node-tile owner gather: each row written once, deterministic;
-                                  writes every owned row completely (accumulate must be 0)          */
+/* ---- scatter modes ("(atomic) increment") — determinism is part of the mode, not a setting:
+ * FEM_SCATTER_ATOMIC     element-parallel, fp64 atomicAdd into values/rhs; summation order varies run to run.
+ * FEM_SCATTER_COLOURED   element colours (no two elements of a colour share a point) in fixed order, plain
+ *                        read-modify-write: bit-identical run to run.
+ * FEM_SCATTER_TILED      owner gather: each CTA owns a set of points and sums every contribution to their rows
+ *                        in shared memory in a FIXED order (per-row turns in record order, or colour runs), then
+ *                        writes every owned row once (no clear pass; accumulate must be 0): bit-identical run to
+ *                        run.  Q1-hex elasticity on lattice meshes takes the z-sweep schedule, other meshes
+ *                        node tiles.  Residual-only calls on tetrahedra use the coloured element pass (cheaper
+ *                        than the tiles for rows alone; still deterministic).  FEM_E_UNSUPPORTED (never a silent
+ *                        fallback) for elements without a tile kernel (quadratic cubes) or a tile point touched
+ *                        by more than 255 visits.
+ * FEM_SCATTER_TILED_UNORDERED  owner gather with shared-memory fp64 atomics where a kernel has them (P2 and
+ *                        NS tets, generic tiles; hex as TILED): faster, summation order varies run to run.
+ *                        Residual-only calls on tetrahedra use the atomic element pass. */
+#define FEM_SCATTER_ATOMIC 0
+#define FEM_SCATTER_COLOURED 1
+#define FEM_SCATTER_TILED 2
+#define FEM_SCATTER_TILED_UNORDERED 3
 
 #define FEM_TIME_STATIC 0
 #define FEM_TIME_GENALPHA 1
@@ -224,10 +238,11 @@ int fem_get_status(fem_mesh_t mesh, void* stream, int64_t* bad_elem);
 int fem_mesh_info(fem_mesh_t mesh, int* n_loc, int* kappa_hat, int* n_colours, int64_t* n_tiles);
 
 /* fem_pattern_info — host query of the node-tile schedule built with the pattern:
- * out[0] tiles, [1] largest tile (points), [2] largest accumulator (doubles), [3] largest packed record
- * (bytes), [4] largest halo (points), [5] element visits in total, [6] largest per-tile visit count,
- * [7] total packed record bytes. */
-int fem_pattern_info(fem_pattern_t pat, int64_t* out8);
+ * out[0] tiles (sweep: steps), [1] largest tile (points; sweep: ring rows), [2] largest accumulator
+ * (doubles), [3] largest packed record (bytes), [4] largest halo (points), [5] element visits in total,
+ * [6] largest per-tile visit count, [7] total packed record bytes, [8] schedule: 0 node tiles, 1 z-sweep,
+ * -1 none (tiled calls return FEM_E_UNSUPPORTED).  out has 9 entries. */
+int fem_pattern_info(fem_pattern_t pat, int64_t* out9);
 
 /* ---- NEXT-1: the linear solve of the Newton sub-step, D-4 ----------------
  * The linearisation K Δφ = -d of d(φ) = 0 is solved on the CSR of fem_pattern_build.

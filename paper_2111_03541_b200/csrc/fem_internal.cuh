@@ -198,7 +198,7 @@ int launch_generic(const AsmArgs& A, bool facet);
 // z-sweep schedule for Q1-hex elasticity on lattice meshes (sweep.cu); FEM_E_UNSUPPORTED: not applicable
 int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s);
 int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_problem* prob,
-                 const double* state, double* values, double* rhs, cudaStream_t stream);
+                 const double* state, double* values, double* rhs, bool det, cudaStream_t stream);
 int pattern_build(fem_mesh_s* m, cudaStream_t stream, fem_pattern_s* p);
 int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t stream);
 void tiles_free(TileSchedule& T);

@@ -292,69 +292,6 @@ __device__ __forceinline__ void hex_visit(const TiledParams& P, const HexView& S
   }
 }
 
-template <int KH, bool DET>
-__global__ void __launch_bounds__(TILED_THREADS, 1) k_hex_tiled(const __grid_constant__ TiledParams P) {
-  using C = TileCfg<ET_HEX, 1, KH, 2>;
-  extern __shared__ __align__(16) unsigned char smem[];
-  TileSmem S = tile_smem_layout<8>(smem, P, C::WARPS);
-  const int64_t tile = blockIdx.x;
-  tile_prologue<KH>(P, S, tile);
-  HexCoef H = {0, 0, 0, 0, 0, 0};
-  for (int f = 0; f < P.n_dom; f++) {
-    const FormArgs& F = P.dom[f];
-    H.cl += F.f0 * F.lam; H.cm += F.f0 * F.mu; H.sl += F.lam; H.sm += F.mu;
-    H.kf0 += F.p[1] * F.f0;
-    if (F.nu_hat >= 1) H.Cf1 += F.p[0] * F.f1;
-  }
-  const int warp = threadIdx.x >> 5;
-  __syncthreads();
-  load_halo<3>(P, S, tile);
-  const int nv = load_visits<8, false>(P, P.dvis, tile, S);
-  const HexView V{S.vown, reinterpret_cast<const uint16_t*>(S.vhal), S.vid, nullptr, S.hdat, S.H,
-                  S.tdeg, S.toff, S.acc, S.racc, S.T};
-  if constexpr (DET) {
-    const int64_t rb = P.dvis.roff[tile], re = P.dvis.roff[tile + 1];
-    const int64_t vbase = P.dvis.run[rb];
-    for (int64_t r = rb; r < re; r++) {  // colour runs: conflict-free, plain shared-memory adds
-      const int v0 = (int)(P.dvis.run[r] - vbase), v1 = (int)(P.dvis.run[r + 1] - vbase);
-      for (int v = v0 + warp; v < v1; v += C::WARPS) hex_visit<KH, true>(P, V, H, v);
-      __syncthreads();
-    }
-  } else {  // warps flow freely; shared-memory fp64 atomics resolve the rare conflicts
-    for (int v = warp; v < nv; v += C::WARPS) hex_visit<KH, false>(P, V, H, v);
-  }
-  unsigned char* slot = S.qp + (size_t)P.rec_bytes * warp;
-  tile_facets<ET_HEX, 1, KH, 2>(P, S, tile, slot);
-  tile_epilogue<KH>(P, S);
-}
-
-template <int KH, bool DET>
-static int run_hex(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
-  using C = TileCfg<ET_HEX, 1, KH, 2>;
-  P.rec_bytes = (int)((sizeof(typename C::QPG) * C::NQF + 15) / 16 * 16);
-  int vmax = (int)T.dom.max_per_tile;
-  for (int f = 0; f < P.n_fac; f++) vmax = std::max<int>(vmax, (int)P.fvis[f].max_per_tile);
-  P.vmax = std::max(vmax, 1);
-  P.hmax = (int)std::max<int64_t>(T.max_halo, 1);
-  P.hcomp = 3 + KH * (P.nu_hat >= 1 ? 2 : 1);
-  P.halo_off = T.halo_off;
-  P.halo_node = T.halo_node;
-  const size_t vis_bytes = (size_t)P.vmax * (4 + 1) + (size_t)P.vmax * 8 * (4 + 2 + 2) + 32;
-  const size_t halo_bytes = ((4 * (size_t)P.hmax + 15) / 16) * 16 + 8 * (size_t)P.hmax * P.hcomp;
-  const size_t uni = std::max(halo_bytes, (size_t)P.rec_bytes * C::WARPS) + 16;
-  const size_t smem = C::HEAD_BYTES + uni + vis_bytes + 16 +
-                      sizeof(double) * ((P.values ? T.acc_max : 0) + (size_t)KH * T.max_tile_nodes);
-  if (smem > 227 * 1024) {
-    set_error("hex tiled kernel: shared memory request too large (" + std::to_string(smem) + " B)");
-    return FEM_E_UNSUPPORTED;
-  }
-  FEM_CUDA_TRY(cudaFuncSetAttribute(k_hex_tiled<KH, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (T.n_tiles <= 0) return 0;
-  k_hex_tiled<KH, DET><<<(unsigned)T.n_tiles, TILED_THREADS, smem, s>>>(P);
-  FEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
 constexpr int FACET_WARPS = 8;  // warps that take part in the (small) facet phase
 constexpr int HEX_MAX_VISITS = 256;  // domain visits of one tile when boundary terms run inside the visits
 constexpr int HEX_SCRATCH = 200;  // doubles of per-warp scratch of hex_visit_el2 (aliases the facet slots)
@@ -382,151 +319,6 @@ __device__ __forceinline__ GeoFrag geo_frag() {
       F.b[s][t] = g[j];
     }
   return F;
-}
-
-// Lean elasticity visit (κ̂ = 3).  Geometry as one GEMM on the fp64 tensor cores:
-//   [J(q) | ∇̂d(q)]_{r,(q,j)} = Σ_a [x_a; d_a]_r ∇̂N_a(ξ_q)_j   (6 x 8) · (8 x 24)  = 6 DMMA,
-// then per point (lanes q = l>>2): J^{-1}, w = det J, ∇d = ∇̂d J^{-1}, S = w σ; the per-point records
-// go through a per-warp shared scratch to the fragment layout (a = l>>2, points c, c+4) for the Gram
-// tiles (18 DMMA) and the residual rows.
-template <bool DET>
-__device__ __forceinline__ void hex_visit_el(const TiledParams& P, const HexView& S, const HexCoef& H,
-                                             const GeoFrag& GF, double* sc, int v) {
-  const int lane = threadIdx.x & 31;
-  const int16_t* own = S.vown + v * 8;
-  const uint16_t* hv = S.vhal + v * 8;
-  const int HH = S.H;
-  const int c = lane & 3, r = lane >> 2;
-  // ---- geometry GEMM: A[r][a] = component r of point a (x,y,z,d1,d2,d3; rows 6,7 zero)
-  double C3[3][2];
-#pragma unroll
-  for (int t = 0; t < 3; t++) { C3[t][0] = 0.0; C3[t][1] = 0.0; }
-#pragma unroll
-  for (int s = 0; s < 2; s++) {
-    const double av = r < 6 ? S.hdat[r * HH + hv[4 * s + c]] : 0.0;
-#pragma unroll
-    for (int t = 0; t < 3; t++) dmma884(C3[t], av, GF.b[s][t]);
-  }
-  if (r < 6) {
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-      sc[r * 24 + 8 * t + 2 * c] = C3[t][0];
-      sc[r * 24 + 8 * t + 2 * c + 1] = C3[t][1];
-    }
-  }
-  __syncwarp();
-  // ---- per point q = lane >> 2 (4 lanes per point compute the same values)
-  const int q = r;
-  double J[3][3], Dr[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; i++)
-#pragma unroll
-    for (int j = 0; j < 3; j++) {
-      J[i][j] = sc[i * 24 + 3 * q + j];
-      Dr[i][j] = sc[(3 + i) * 24 + 3 * q + j];
-    }
-  const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
-  const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
-  const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
-  const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-  if (__any_sync(0xffffffffu, !(det > 0.0))) {
-    if (lane == 0) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)S.velem[v]);
-    return;
-  }
-  const double rr = 1.0 / det;
-  double Ji[3][3];
-  Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
-  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
-  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
-  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
-  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
-  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
-  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
-  double gu[3][3];
-#pragma unroll
-  for (int k = 0; k < 3; k++)
-#pragma unroll
-    for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
-  __syncwarp();  // everyone has read the GEMM output; the scratch now takes the per-point records
-  if (c == 0) {
-    double* o = sc + q * 20;
-#pragma unroll
-    for (int j = 0; j < 3; j++)
-#pragma unroll
-      for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
-    o[9] = det;  // w (unit Gauss-Legendre weights)
-    const double lw = H.sl * det * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * det;
-#pragma unroll
-    for (int i = 0; i < 3; i++)
-#pragma unroll
-      for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
-  }
-  __syncwarp();
-  // ---- fragment layout: node a = lane >> 2, points c and c + 4
-  const int a = r;
-  const double* o0 = sc + c * 20;
-  const double* o1 = sc + (c + 4) * 20;
-  double g0[3], g1[3], N0, N1, G0[3], G1[3];
-  hex_ref(a, c, g0, N0);
-  hex_ref(a, c + 4, g1, N1);
-#pragma unroll
-  for (int i = 0; i < 3; i++) {
-    G0[i] = o0[0 * 3 + i] * g0[0] + o0[1 * 3 + i] * g0[1] + o0[2 * 3 + i] * g0[2];
-    G1[i] = o1[0 * 3 + i] * g1[0] + o1[1 * 3 + i] * g1[1] + o1[2 * 3 + i] * g1[2];
-  }
-  const double w0 = o0[9], w1 = o1[9];
-  const int li = own[a];
-  if (P.rhs) {  // r_(a,i) = -Σ_γ w σ_ij G_aj
-    double res[3];
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-      double t = 0.0;
-#pragma unroll
-      for (int j = 0; j < 3; j++) {
-        t = fma(o0[10 + i * 3 + j], G0[j], t);
-        t = fma(o1[10 + i * 3 + j], G1[j], t);
-      }
-      res[i] = -sum4(t);
-    }
-    if (c == 0 && li >= 0) {
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        if constexpr (DET) S.racc[i * S.T + li] += res[i];
-        else atomicAdd(S.racc + i * S.T + li, res[i]);
-      }
-    }
-  }
-  if (P.values) {
-    double M[3][3][2];
-#pragma unroll
-    for (int j = 0; j < 3; j++)
-#pragma unroll
-      for (int k = 0; k < 3; k++) {
-        M[j][k][0] = 0.0;
-        M[j][k][1] = 0.0;
-        dmma884(M[j][k], w0 * G0[j], G0[k]);
-        dmma884(M[j][k], w1 * G1[j], G1[k]);
-      }
-    if (li >= 0) {
-      const int d = S.tdeg[li], sr = acc_row_stride(3, d, P.nnz_s);
-      double* base = S.acc + S.toff[li];
-      const uint8_t* lc = S.vloc + v * 64 + a * 8 + 2 * c;
-#pragma unroll
-      for (int t = 0; t < 2; t++) {
-        const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
-        double* rowb = base + lc[t];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-#pragma unroll
-          for (int m = 0; m < 3; m++) {
-            const double kv = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
-            if constexpr (DET) rowb[i * sr + m * d] += kv;
-            else atomicAdd(rowb + i * sr + m * d, kv);
-          }
-      }
-    }
-  }
-  __syncwarp();  // scratch is reused by the next visit
 }
 
 // ---- persistent record-driven kernel: one CTA per SM walks the tiles; the next tile's packed record
@@ -1407,9 +1199,9 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)KH * T.max_tile_nodes);
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
   P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
-  P.spin_ns = getenv("FEM_SPIN_NS") ? atoi(getenv("FEM_SPIN_NS")) : 0;
+  P.spin_ns = 0;
   // elasticity boundary terms (fix / load) inside the owning element's visit: no facet phase, no barriers
-  P.fac_inline = KH == 3 && T.dom.max_per_tile <= HEX_MAX_VISITS && !getenv("FEM_HEX_FACET_PHASE");
+  P.fac_inline = KH == 3 && T.dom.max_per_tile <= HEX_MAX_VISITS;
   for (int f = 0; f < P.n_fac; f++) {
     const int fo = P.fac[f].form;
     if ((fo != FEM_WF_ELAST_FIX_ALL && fo != FEM_WF_ELAST_FIX_D1 && fo != FEM_WF_ELAST_LOAD) || P.fac_set[f] > 4)
@@ -1438,6 +1230,15 @@ static int run_hex_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
 // Q1 hex, 2x2x2 points, domain terms all ELAST_DOMAIN (κ̂ = 3) or all THERMAL_DOMAIN (κ̂ = 1).
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled) {
   *handled = false;
+  if (T.sweep) {  // sweep records are read only by the sweep kernel
+    *handled = true;
+    for (int f = 0; f < P.n_dom; f++)
+      if (P.dom[f].form != FEM_WF_ELAST_DOMAIN) {
+        set_error("tiled scatter: the sweep schedule of this mesh takes the elasticity domain form only");
+        return FEM_E_UNSUPPORTED;
+      }
+    return run_hex_sweep(P, T, s);  // ordered: deterministic in both tiled modes
+  }
   if (P.n_dom == 0) return 0;
   for (int f = 0; f < P.n_dom; f++) {
     if (kh == 3 && P.dom[f].form != FEM_WF_ELAST_DOMAIN) return 0;
@@ -1445,19 +1246,13 @@ int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cu
   }
   if (kh != 1 && kh != 3) return 0;
   *handled = true;
-  if (T.sweep) {
-    if (kh != 3 || !det) {
-      set_error("hex sweep schedule: ordered elasticity only");
-      return FEM_E_UNSUPPORTED;
-    }
-    return run_hex_sweep(P, T, s);
+  if (det && kh == 3 && T.max_turns > 255) {
+    set_error("tiled scatter: a tile point is touched by more than 255 element visits (8-bit turns); use "
+              "FEM_SCATTER_COLOURED or FEM_SCATTER_TILED_UNORDERED");
+    return FEM_E_UNSUPPORTED;
   }
-  if (T.rec && !getenv("FEM_NO_RECORDS")) {
-    if (det) return kh == 3 ? run_hex_rec<3, true>(P, T, s) : run_hex_rec<1, true>(P, T, s);
-    return kh == 3 ? run_hex_rec<3, false>(P, T, s) : run_hex_rec<1, false>(P, T, s);
-  }
-  if (det) return kh == 3 ? run_hex<3, true>(P, T, s) : run_hex<1, true>(P, T, s);
-  return kh == 3 ? run_hex<3, false>(P, T, s) : run_hex<1, false>(P, T, s);
+  if (det) return kh == 3 ? run_hex_rec<3, true>(P, T, s) : run_hex_rec<1, true>(P, T, s);
+  return kh == 3 ? run_hex_rec<3, false>(P, T, s) : run_hex_rec<1, false>(P, T, s);
 }
 
 }  // namespace fem

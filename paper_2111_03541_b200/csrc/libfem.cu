@@ -281,7 +281,7 @@ int fem_pattern_build(fem_mesh_t m, void* stream, fem_pattern_t* out, int64_t* n
     // Q1-hex elasticity on a node lattice (c5 and its perturbed variant): the z-sweep schedule (sweep.cu),
     // 1.36 element visits per element instead of the node tiles' 1.95; other meshes: node tiles
     int trc = FEM_E_UNSUPPORTED;
-    if (m->etype == FEM_HEX && m->order == 1 && m->kh == 3 && !getenv("FEM_NO_SWEEP"))
+    if (m->etype == FEM_HEX && m->order == 1 && m->kh == 3)
       trc = sweep_build(m, p, (cudaStream_t)stream);
     if (trc == FEM_E_OOM || trc == FEM_E_CUDA) { fem_pattern_destroy(p); return trc; }
     if (trc != 0) {
@@ -309,6 +309,7 @@ int fem_pattern_info(fem_pattern_t p, int64_t* out) {
   const TileSchedule& T = p->tiles;
   out[0] = T.n_tiles; out[1] = T.max_tile_nodes; out[2] = T.acc_max; out[3] = T.rec_max;
   out[4] = T.max_halo; out[5] = T.visits_total; out[6] = T.dom.max_per_tile; out[7] = T.rec_bytes_total;
+  out[8] = p->tiles_rc ? -1 : (T.sweep ? 1 : 0);
   return 0;
 }
 
@@ -361,23 +362,22 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   bool bnd_only = false;  // tiled NS: domain terms in the tile kernel, boundary terms coloured afterwards
-  if (scatter == FEM_SCATTER_TILED && !values && m->etype == FEM_TET && !getenv("FEM_NS_DET") &&
-      !getenv("FEM_TILED_RESIDUAL")) {
-    // residual-only on tets: the tile kernels visit each element ~3x (24 elements per vertex) and their
-    // shared-memory sums are atomic (not ordered) anyway, so the element pass with fp64 RED into the
-    // (L2-sized) rhs is the faster unordered path (c3 3.0 -> 0.9 ms, c4 25 -> 12.5 ms)
-    scatter = FEM_SCATTER_ATOMIC;
-    accumulate = 0;
-  }
-  if (scatter == FEM_SCATTER_TILED) {
-    if (accumulate) { set_error("tiled scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
+  const bool tiled = scatter == FEM_SCATTER_TILED || scatter == FEM_SCATTER_TILED_UNORDERED;
+  if (tiled && accumulate) { set_error("tiled scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
+  if (tiled && !values && m->etype == FEM_TET) {
+    // residual-only calls on tetrahedra: the tile kernels visit each element ~3x (24 elements per vertex)
+    // for rows that are cheap to scatter, so these calls take the element pass instead (documented in
+    // libfem.h): coloured (deterministic) for FEM_SCATTER_TILED, atomic for _UNORDERED (c3 3.0 -> 0.9 ms)
+    scatter = scatter == FEM_SCATTER_TILED ? FEM_SCATTER_COLOURED : FEM_SCATTER_ATOMIC;
+  } else if (tiled) {
     if (!p) { set_error("tiled scatter needs the pattern"); return FEM_E_INVALID_ARG; }
     if (p->tiles_rc) { set_error(p->tiles_msg); return p->tiles_rc; }
+    const bool det = scatter == FEM_SCATTER_TILED;
     // NS on P1 tets: the generic boundary terms (1% of the visits) would stall the whole tile
     // behind a facet phase run by a few warps (22% of c4); they run instead as the deterministic coloured
-    // facet pass over the rows the tile kernel has written (FEM_NS_FACET_PHASE=1 keeps the in-tile phase)
-    const bool ns_split = m->etype == FEM_TET && m->order == 1 && m->physics == FEM_NS && !getenv("FEM_NS_FACET_PHASE");
-    if (!ns_split) return launch_tiled(m, p, prob, state, values, rhs, s);
+    // facet pass over the rows the tile kernel has written
+    const bool ns_split = m->etype == FEM_TET && m->order == 1 && m->physics == FEM_NS;
+    if (!ns_split) return launch_tiled(m, p, prob, state, values, rhs, det, s);
     fem_problem dom = *prob;
     dom.n_terms = 0;
     bool any_bnd = false;
@@ -385,16 +385,20 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
       if (prob->terms[t].region < 0) dom.terms[dom.n_terms++] = prob->terms[t];
       else any_bnd = true;
     }
-    rc = launch_tiled(m, p, &dom, state, values, rhs, s);
+    rc = launch_tiled(m, p, &dom, state, values, rhs, det, s);
     if (rc || !any_bnd) return rc;
     bnd_only = true;
     scatter = FEM_SCATTER_COLOURED;
-  } else if (scatter != FEM_SCATTER_ATOMIC && scatter != FEM_SCATTER_COLOURED) {
-    set_error("bad scatter mode");
-    return FEM_E_INVALID_ARG;
-  } else if (!accumulate) {  // "cleared first" (D-2 P:426, D-3 P:441)
-    if (values) FEM_CUDA_TRY(cudaMemsetAsync(values, 0, sizeof(double) * p->nnz, s));
-    if (rhs) FEM_CUDA_TRY(cudaMemsetAsync(rhs, 0, sizeof(double) * m->kh * m->n_own, s));
+  }
+  if (!tiled || scatter == FEM_SCATTER_COLOURED || scatter == FEM_SCATTER_ATOMIC) {
+    if (scatter != FEM_SCATTER_ATOMIC && scatter != FEM_SCATTER_COLOURED) {
+      set_error("bad scatter mode");
+      return FEM_E_INVALID_ARG;
+    }
+    if (!accumulate && !bnd_only) {  // "cleared first" (D-2 P:426, D-3 P:441)
+      if (values) FEM_CUDA_TRY(cudaMemsetAsync(values, 0, sizeof(double) * p->nnz, s));
+      if (rhs) FEM_CUDA_TRY(cudaMemsetAsync(rhs, 0, sizeof(double) * m->kh * m->n_own, s));
+    }
   }
   for (int t = 0; t < prob->n_terms; t++) {
     const fem_term& T = prob->terms[t];

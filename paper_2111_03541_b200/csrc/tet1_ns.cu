@@ -328,6 +328,11 @@ int launch_ns_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_
   *handled = false;
   if (P.n_dom != 1 || P.dom[0].form != FEM_WF_NS_DOMAIN || !T.rec) return 0;
   *handled = true;
+  if (det && T.max_turns > 255) {
+    set_error("tiled scatter: a tile point is touched by more than 255 element visits (8-bit turns); use "
+              "FEM_SCATTER_COLOURED or FEM_SCATTER_TILED_UNORDERED");
+    return FEM_E_UNSUPPORTED;
+  }
   using C = TileCfg<ET_TET, 1, 4, 2>;
   constexpr int NL = 4;
   P.rec_bytes = (int)((sizeof(typename C::QPG) * C::NQF + 15) / 16 * 16);

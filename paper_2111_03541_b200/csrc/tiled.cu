@@ -29,24 +29,15 @@ namespace fem {
 
 constexpr int64_t ACC_BUDGET_MAX = 16384;  // doubles (128 KB): hard cap of the row accumulator
 // Cap on element visits per tile (bounds the packed record, double-buffered in shared memory).
-static int64_t tile_visit_cap(int NL) {
-  const char* s = getenv("FEM_TILE_VISITS");
-  if (s) return atoll(s);
-  return NL == 8 ? 144 : (NL == 10 ? 240 : 640);
-}
+static int64_t tile_visit_cap(int NL) { return NL == 8 ? 144 : (NL == 10 ? 240 : 640); }
 // Cap on halo points per tile (bounds the staged coordinates/state, double-buffered).
-static int64_t tile_halo_cap(int NL) {
-  const char* s = getenv("FEM_TILE_HALO");
-  if (s) return atoll(s);
-  return NL == 8 ? 300 : (NL == 10 ? 480 : 640);
-}
+static int64_t tile_halo_cap(int NL) { return NL == 8 ? 300 : (NL == 10 ? 480 : 640); }
 
 // Accumulator budget (doubles).  κ̂ = 1 rows are short, so a tile would hold hundreds of points and
 // its packed record (double-buffered in shared memory) would not fit: cap it at 4096 doubles.
 static int64_t acc_budget(int kh, int nl) {
-  const char* s = getenv("FEM_TILE_ACC");
   // P2 tets: 144 B of visit data per element, so the double-buffered records need room too
-  int64_t x = s ? atoll(s) : (kh == 1 ? 4096 : (nl == 10 ? 8192 : 16384));
+  int64_t x = kh == 1 ? 4096 : (nl == 10 ? 8192 : 16384);
   return x < 256 ? 256 : (x > ACC_BUDGET_MAX ? ACC_BUDGET_MAX : x);
 }
 
@@ -561,27 +552,6 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
   return 0;
 }
 
-template <int ET, int ORD, int KH, int Q>
-__global__ void __launch_bounds__(TILED_THREADS, 1) k_tiled(const __grid_constant__ TiledParams P) {
-  using C = TileCfg<ET, ORD, KH, Q>;
-  constexpr int NL = C::NL;
-  extern __shared__ __align__(16) unsigned char smem[];
-  TileSmem S = tile_smem_layout<NL>(smem, P, C::WARPS);
-  const int64_t tile = blockIdx.x;
-  tile_prologue<KH>(P, S, tile);
-  const int warp = threadIdx.x >> 5;
-  unsigned char* slot = S.qp + (size_t)P.rec_bytes * warp;
-  {
-    const int nv = load_visits<NL, false>(P, P.dvis, tile, S);  // (its first barrier also covers the zeroing)
-    if (P.lean)
-      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, S, v, slot);
-    else
-      for (int v = warp; v < nv; v += C::WARPS) warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, S, v, slot);
-  }
-  tile_facets<ET, ORD, KH, Q>(P, S, tile, slot);
-  tile_epilogue<KH>(P, S);
-}
-
 // ---- persistent record-driven generic kernel (tets, triangles, hex with other forms): the next tile's
 // packed record arrives by one TMA bulk copy while the current tile computes; the tile's halo points
 // (coordinates + state) are staged in shared memory once per tile; warps take element visits freely
@@ -600,7 +570,11 @@ __device__ __forceinline__ void gather_halo_gen(const TiledParams& P, const uint
   cp_async_commit();
 }
 
-template <int ET, int ORD, int KH, int Q>
+// DET: the visits of a colour run share no point, so within a run every accumulator entry receives at most
+// one contribution; runs are separated by block barriers and boundary facets go by node-disjoint segments
+// (rec_facets): the sums have a fixed order, bit-identical run to run.  !DET: warps grab visits freely and
+// shared-memory fp64 atomics resolve the conflicts (FEM_SCATTER_TILED_UNORDERED).
+template <int ET, int ORD, int KH, int Q, bool DET>
 __global__ void __launch_bounds__(TILED_THREADS, 1) k_gen_rec(const __grid_constant__ TiledParams P) {
   using C = TileCfg<ET, ORD, KH, Q>;
   constexpr int NL = C::NL, DIM = C::DIM;
@@ -673,19 +647,32 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_gen_rec(const __grid_const
     if (tid == 0) *ctr = 0;
     cp_async_wait_all();
     __syncthreads();
-    if (P.lean)
-      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1))
-        warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, D, v, slot);
-    else
-      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1))
-        warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, D, v, slot);
-    if (fmask) rec_facets<ET, ORD, KH, Q, C::WARPS>(P, D, rec, L, slot);
+    if constexpr (DET) {
+      const int32_t* run = reinterpret_cast<const int32_t*>(rec + L.o_run);
+      for (int r = 0; r < nr; r++) {
+        if (P.lean)
+          for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS)
+            warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, D, v, slot);
+        else
+          for (int v = run[r] + warp; v < run[r + 1]; v += C::WARPS)
+            warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, D, v, slot);
+        __syncthreads();
+      }
+    } else {
+      if (P.lean)
+        for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1))
+          warp_visit<ET, ORD, KH, Q, false, true>(P, P.dom, P.n_dom, D, v, slot);
+      else
+        for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1))
+          warp_visit<ET, ORD, KH, Q, false, false>(P, P.dom, P.n_dom, D, v, slot);
+    }
+    if (fmask) rec_facets<ET, ORD, KH, Q, C::WARPS, DET>(P, D, rec, L, slot);
     tile_epilogue<KH>(P, D);
     __syncthreads();
   }
 }
 
-template <int ET, int ORD, int KH, int Q>
+template <int ET, int ORD, int KH, int Q, bool DET>
 static int run_gen_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
   using C = TileCfg<ET, ORD, KH, Q>;
   constexpr int NL = C::NL, DIM = C::DIM;
@@ -711,56 +698,34 @@ static int run_gen_rec(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
     set_error("record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
     return FEM_E_UNSUPPORTED;
   }
-  FEM_CUDA_TRY(cudaFuncSetAttribute(k_gen_rec<ET, ORD, KH, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  FEM_CUDA_TRY(cudaFuncSetAttribute(k_gen_rec<ET, ORD, KH, Q, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (T.n_tiles <= 0) return 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
-  k_gen_rec<ET, ORD, KH, Q><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  k_gen_rec<ET, ORD, KH, Q, DET><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
-template <int ET, int ORD, int KH, int Q>
-static int run_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s) {
-  using C = TileCfg<ET, ORD, KH, Q>;
-  if (T.rec && getenv("FEM_GEN_RECORDS")) return run_gen_rec<ET, ORD, KH, Q>(P, T, s);
-  constexpr int NL = C::NL;
-  const size_t rec_dom = (P.lean ? sizeof(typename C::QPL) : sizeof(typename C::QPG)) * C::NQV;
-  const size_t rec_fac = sizeof(typename C::QPG) * C::NQF;
-  P.rec_bytes = (int)((std::max(rec_dom, rec_fac) + 15) / 16 * 16);
-  int vmax = (int)T.dom.max_per_tile;
-  for (int f = 0; f < P.n_fac; f++) vmax = std::max<int>(vmax, (int)P.fvis[f].max_per_tile);
-  vmax = std::max(vmax, 1);
-  P.vmax = vmax;
-  const size_t vis_bytes = (size_t)vmax * (4 + 1) + (size_t)vmax * NL * (4 + 2) + 32;
-  const size_t smem = C::HEAD_BYTES + (size_t)P.rec_bytes * C::WARPS + vis_bytes + 16 +
-                      sizeof(double) * ((P.values ? T.acc_max : 0) + (size_t)KH * T.max_tile_nodes);
-  if (smem > 227 * 1024) {
-    set_error("tiled kernel: shared memory request too large (" + std::to_string(smem) + " B)");
+template <int ET, int ORD, int KH, bool DET>
+static int run_tiled_q(int q, TiledParams& P, const TileSchedule& T, cudaStream_t s) {
+  if (!T.rec) {
+    set_error("tiled: no tile records");
     return FEM_E_UNSUPPORTED;
   }
-  FEM_CUDA_TRY(cudaFuncSetAttribute(k_tiled<ET, ORD, KH, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (T.n_tiles <= 0) return 0;
-  k_tiled<ET, ORD, KH, Q><<<(unsigned)T.n_tiles, TILED_THREADS, smem, s>>>(P);
-  FEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-template <int ET, int ORD, int KH>
-static int run_tiled_q(int q, TiledParams& P, const TileSchedule& T, cudaStream_t s) {
-  if (q == 1) return run_tiled<ET, ORD, KH, 1>(P, T, s);
-  if (q == 2) return run_tiled<ET, ORD, KH, 2>(P, T, s);
+  if (q == 1) return run_gen_rec<ET, ORD, KH, 1, DET>(P, T, s);
+  if (q == 2) return run_gen_rec<ET, ORD, KH, 2, DET>(P, T, s);
   if constexpr (ET == ET_HEX) {
-    if (q == 3) return run_tiled<ET, ORD, KH, 3>(P, T, s);
+    if (q == 3) return run_gen_rec<ET, ORD, KH, 3, DET>(P, T, s);
   }
   set_error("tiled: unsupported quadrature order");
   return FEM_E_UNSUPPORTED;
 }
 
 int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_problem* prob, const double* state,
-                 double* values, double* rhs, cudaStream_t s) {
+                 double* values, double* rhs, bool det, cudaStream_t s) {
   const TileSchedule& T = pat->tiles;
   TiledParams P;
   memset(&P, 0, sizeof(P));
@@ -789,43 +754,44 @@ int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_proble
   P.values = values; P.rhs = rhs; P.err = m->err;
   P.nu_hat = prob->time.kind == FEM_TIME_GENALPHA ? prob->time.nu_hat : 0;
   const int et = m->etype, o = m->order, kh = m->kh, q = prob->quad_order;
-  // ordered (bit-identical run to run) unless FEM_TILED_NONDET asks for the atomic variant; per-row turn
-  // numbers are bytes, so a tile point touched by more than 256 visits takes the atomic variant
-  const bool det = getenv("FEM_TILED_NONDET") == nullptr && T.max_turns <= 256;
-  if (et == ET_HEX && o == 1 && q == 2 && !getenv("FEM_NO_HEX_MMA")) {
+  // det (FEM_SCATTER_TILED): bit-identical run to run — ordered per-row turns (hex, NS) or colour runs
+  // (generic); !det (FEM_SCATTER_TILED_UNORDERED): shared-memory fp64 atomics where a kernel has them
+  if (et == ET_HEX && o == 1 && q == 2) {
     bool handled = false;
     const int rc = launch_hex_tiled(P, T, kh, det, s, &handled);
     if (handled) return rc;
   }
-  if (et == ET_TET && o == 1 && kh == 4 && q == 2 && !getenv("FEM_NO_NS_SPEC")) {
+  if (et == ET_TET && o == 1 && kh == 4 && q == 2) {
     bool handled = false;
-    // ordered turns cost ~25% on tets (24 elements per vertex: consecutive visits share rows), so the
-    // NS kernel is ordered only on request (FEM_NS_DET); the coloured scatter is deterministic too
-    const int rc = launch_ns_tiled(P, T, det && getenv("FEM_NS_DET") != nullptr, s, &handled);
+    // ordered turns cost ~25% on c4 (24 elements per vertex: consecutive visits share rows)
+    const int rc = launch_ns_tiled(P, T, det, s, &handled);
     if (handled) return rc;
   }
-  if (et == ET_TET && o == 2 && kh == 3 && q == 2 && !getenv("FEM_NO_P2_SPEC")) {
+  if (!det && et == ET_TET && o == 2 && kh == 3 && q == 2) {  // P2 elasticity: atomic-accumulating kernel
     bool handled = false;
     const int rc = launch_p2_tiled(P, T, s, &handled);
     if (handled) return rc;
   }
+#define FEM_GEN(ET_, ORD_, KH_) \
+  return det ? run_tiled_q<ET_, ORD_, KH_, true>(q, P, T, s) : run_tiled_q<ET_, ORD_, KH_, false>(q, P, T, s)
   if (et == ET_TRI && o == 1) {
-    if (kh == 1) return run_tiled_q<ET_TRI, 1, 1>(q, P, T, s);
-    if (kh == 2) return run_tiled_q<ET_TRI, 1, 2>(q, P, T, s);
+    if (kh == 1) FEM_GEN(ET_TRI, 1, 1);
+    if (kh == 2) FEM_GEN(ET_TRI, 1, 2);
   }
   if (et == ET_HEX && o == 1) {
-    if (kh == 1) return run_tiled_q<ET_HEX, 1, 1>(q, P, T, s);
-    if (kh == 3) return run_tiled_q<ET_HEX, 1, 3>(q, P, T, s);
+    if (kh == 1) FEM_GEN(ET_HEX, 1, 1);
+    if (kh == 3) FEM_GEN(ET_HEX, 1, 3);
   }
   if (et == ET_TET && o == 1) {
-    if (kh == 1) return run_tiled_q<ET_TET, 1, 1>(q, P, T, s);
-    if (kh == 3) return run_tiled_q<ET_TET, 1, 3>(q, P, T, s);
-    if (kh == 4) return run_tiled_q<ET_TET, 1, 4>(q, P, T, s);
+    if (kh == 1) FEM_GEN(ET_TET, 1, 1);
+    if (kh == 3) FEM_GEN(ET_TET, 1, 3);
+    if (kh == 4) FEM_GEN(ET_TET, 1, 4);
   }
   if (et == ET_TET && o == 2) {
-    if (kh == 1) return run_tiled_q<ET_TET, 2, 1>(q, P, T, s);
-    if (kh == 3) return run_tiled_q<ET_TET, 2, 3>(q, P, T, s);
+    if (kh == 1) FEM_GEN(ET_TET, 2, 1);
+    if (kh == 3) FEM_GEN(ET_TET, 2, 3);
   }
+#undef FEM_GEN
   set_error("tiled: unsupported element/physics combination");
   return FEM_E_UNSUPPORTED;
 }

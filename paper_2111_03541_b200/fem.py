@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("FEM_LIB_PATH") or os.path.join(_HERE, "libfem.so")  #
 
 FEM_TRI, FEM_TET, FEM_HEX, FEM_HEX_SERENDIPITY = 1, 2, 4, 5
 FEM_THERMAL, FEM_ELASTICITY, FEM_NS = 1, 2, 3
-SCATTER = {"atomic": 0, "coloured": 1, "tiled": 2}
+SCATTER = {"atomic": 0, "coloured": 1, "tiled": 2, "tiled_unordered": 3}
 ETYPE = {"tri": FEM_TRI, "tet": FEM_TET, "hex": FEM_HEX, "hexs": FEM_HEX_SERENDIPITY}
 PHYSICS = {"thermal": FEM_THERMAL, "elasticity": FEM_ELASTICITY, "ns": FEM_NS}
 FORM = {
@@ -220,10 +220,10 @@ def fem_pattern_nnz_s(pat_h):
 
 
 def fem_pattern_info(pat_h):
-    out = np.zeros(8, dtype=np.int64)
+    out = np.zeros(9, dtype=np.int64)
     _check(lib().fem_pattern_info(pat_h, out.ctypes.data))
     keys = ["tiles", "max_tile_points", "max_acc_doubles", "max_record_bytes", "max_halo_points", "visits",
-            "max_tile_visits", "record_bytes"]
+            "max_tile_visits", "record_bytes", "schedule"]
     return dict(zip(keys, out.tolist()))
 
 

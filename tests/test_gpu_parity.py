@@ -74,23 +74,41 @@ def test_small_parity_all_modes(name, variant):
     S.close()
 
 
-@pytest.mark.parametrize("name,sc", [(n, "coloured") for n in ("c2", "c3", "c4", "c5")] +
-                         [("c2", "tiled"), ("c5", "tiled"), ("c4", "tiled")])
+@pytest.mark.parametrize("name,sc", [(n, sc) for n in ("c1", "c2", "c3", "c4", "c5") for sc in ("coloured", "tiled")])
 def test_deterministic_modes_bit_exact(name, sc):
-    """Coloured scatter everywhere, and the tiled path on Q1 hex and (FEM_NS_DET) P1 NS tets (per-row
-    turns: every accumulator entry sums its contributions in record order)."""
+    """FEM_SCATTER_COLOURED and FEM_SCATTER_TILED are deterministic by contract (libfem.h) on every element
+    type: hex (sweep / ordered tiles), P1 NS tets (ordered turns), P2 tets and triangles (colour runs).
+    Matrix, residual and the system call are bit-identical call after call."""
     _need_gpu()
     m, p = make_config(name, "perturbed", SMALL[name])
     st = _to_dev(make_state(name, m, p))
     S = _gpu_system(m, p)
-    os.environ["FEM_NS_DET"] = "1"  # read at launch: the NS tile kernel's ordered variant is opt-in
-    try:
-        ref_v, ref_r = [x.clone() for x in S.system(st, scatter=sc)]
-        for _ in range(3):
-            v, r = S.system(st, scatter=sc)
-            assert torch.equal(v, ref_v) and torch.equal(r, ref_r)
-    finally:
-        del os.environ["FEM_NS_DET"]
+    if name == "c5":
+        assert S.info()["schedule"] == 1  # the z-sweep
+    ref_v, ref_r = [x.clone() for x in S.system(st, scatter=sc)]
+    ref_m = S.matrix(st, scatter=sc).clone()
+    ref_res = S.residual(st, scatter=sc).clone()
+    for _ in range(3):
+        v, r = S.system(st, scatter=sc)
+        assert torch.equal(v, ref_v) and torch.equal(r, ref_r)
+        assert torch.equal(S.matrix(st, scatter=sc), ref_m)
+        assert torch.equal(S.residual(st, scatter=sc), ref_res)
+    S.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_tiled_unordered_parity(name):
+    """FEM_SCATTER_TILED_UNORDERED (shared-memory atomics where the kernels have them) agrees with the oracle."""
+    _need_gpu()
+    m, p = make_config(name, "perturbed", SMALL[name])
+    st = make_state(name, m, p)
+    ora = oracle.assemble(m, p, st)
+    S = _gpu_system(m, p)
+    sd = _to_dev(st)
+    for v, r in [S.system(sd, scatter="tiled_unordered"),
+                 (S.matrix(sd, scatter="tiled_unordered").clone(), S.residual(sd, scatter="tiled_unordered").clone())]:
+        assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL
+        assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL
     S.close()
 
 
@@ -150,8 +168,8 @@ def test_genalpha_elasticity_f0(name):
 def test_hex_elasticity_boundary_terms_every_face(variant):
     """Q1 hex elasticity with FIX_D1 / FIX_ALL (non-zero dʷ) / LOAD (full σˡ) on faces of every axis and
     both sides, an element with two boundary faces in one set, and two terms on one set:
-    the tiled kernel integrates them inside the element visits; the generic facet phase
-    (FEM_HEX_FACET_PHASE) and the atomic / coloured paths must agree with the oracle."""
+    the tiled kernels (sweep and node tiles) integrate them inside the element visits; the atomic /
+    coloured paths must agree with the oracle."""
     _need_gpu()
     from fem_inputs.configs import Term
     from fem_inputs.meshgen import facets_on_plane
@@ -170,19 +188,13 @@ def test_hex_elasticity_boundary_terms_every_face(variant):
     st = make_state("c5", m, p)
     ora = oracle.assemble(m, p, st)
     assert ora["status"] == 0
-    for phase in ("", "1"):
-        if phase:
-            os.environ["FEM_HEX_FACET_PHASE"] = phase
-        try:
-            S = _gpu_system(m, p)
-            sd = _to_dev(st)
-            for sc in SCATTERS:
-                for v, r in [S.system(sd, scatter=sc), (S.matrix(sd, scatter=sc).clone(), S.residual(sd, scatter=sc).clone())]:
-                    assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL, (sc, phase)
-                    assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL, (sc, phase)
-            S.close()
-        finally:
-            os.environ.pop("FEM_HEX_FACET_PHASE", None)
+    S = _gpu_system(m, p)
+    sd = _to_dev(st)
+    for sc in SCATTERS:
+        for v, r in [S.system(sd, scatter=sc), (S.matrix(sd, scatter=sc).clone(), S.residual(sd, scatter=sc).clone())]:
+            assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL, sc
+            assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL, sc
+    S.close()
 
 
 def test_inverted_element_reported_and_edge_cases():
@@ -342,3 +354,29 @@ def test_two_workpieces_block_diagonal_coo():
         S.close()
     (s0, I0, J0), (s1, I1, J1) = parts
     assert s1 == len(I0) and I1.min() >= I0.max() + 1 and J1.min() >= J0.max() + 1
+
+
+@pytest.mark.parametrize("sc", ["tiled", "tiled_unordered"])
+def test_hex_elasticity_node_tiles_on_rotated_mesh(sc):
+    """A Q1-hex elasticity mesh that does not bin onto an axis-aligned lattice (c5 rotated by 30° about z
+    and 20° about x) keeps the node-tile schedule (k_hex_rec) instead of the z-sweep: parity with the
+    oracle and, for FEM_SCATTER_TILED, bit-identical repeats."""
+    _need_gpu()
+    m, p = make_config("c5", "perturbed", SMALL["c5"])
+    a, b = np.radians(30.0), np.radians(20.0)
+    Rz = np.array([[np.cos(a), -np.sin(a), 0], [np.sin(a), np.cos(a), 0], [0, 0, 1]])
+    Rx = np.array([[1, 0, 0], [0, np.cos(b), -np.sin(b)], [0, np.sin(b), np.cos(b)]])
+    m.coords = np.ascontiguousarray(Rx @ Rz @ m.coords)
+    st = make_state("c5", m, p)
+    ora = oracle.assemble(m, p, st)
+    assert ora["status"] == 0
+    S = _gpu_system(m, p)
+    assert S.info()["schedule"] == 0  # node tiles
+    sd = _to_dev(st)
+    v, r = [x.clone() for x in S.system(sd, scatter=sc)]
+    assert csr_row_scaled_err(ora["rowptr"], v.cpu().numpy(), ora["values"]) <= TOL
+    assert rhs_err(r.cpu().numpy(), ora["rhs"], ora["abs_d"]) <= TOL
+    if sc == "tiled":
+        v2, r2 = S.system(sd, scatter=sc)
+        assert torch.equal(v, v2) and torch.equal(r, r2)
+    S.close()
