@@ -8,7 +8,8 @@
 //              lane l = 4a + c holds ∇N_{a}(ξ_c) and ∇N_{8+(a&1)}(ξ_c), the A/B fragments of three 8x8
 //              node tiles that with the symmetry of K cover the 10x10 node block: 27 DMMA;
 //   K_(a,i),(b,m) = -f0 (λ M^im + μ M^mi + μ δ_im tr M);  r_(a,i) = -Σ_γ w σ_ij G_aj.
-// Contributions go to the tile accumulator with shared-memory fp64 atomics.
+// Contributions go to the tile accumulator in record order under per-row turns (FEM_SCATTER_TILED,
+// deterministic) or with shared-memory fp64 atomics (FEM_SCATTER_TILED_UNORDERED).
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -30,7 +31,7 @@ __device__ __forceinline__ double sum4_t2(double v) {
 }
 
 struct P2Offs {
-  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc;
+  uint32_t vown, vhal, velem, vloc, hdat, tdeg, toff, acc, racc, vseq, turn;
   int H, T;
 };
 constexpr int P2_LANE_TAB = 12;   // GEMM B fragments (3 k-steps x 2 n-tiles) | ∇̂N_a0(ξ_c) | ∇̂N_{8+(a0&1)}(ξ_c)
@@ -41,8 +42,21 @@ struct P2Coef {
   double cl, cm, sl, sm;  // Σ f0 λ, Σ f0 μ (matrix); Σ λ, Σ μ (residual)
 };
 
-// HAS_V / HAS_R: the call kind (matrix, residual, both) fixed per launch, so each body compiles lean
-template <bool HAS_V, bool HAS_R>
+// acquire / release on a shared-memory turn counter (scope CTA)
+__device__ __forceinline__ int p2_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void p2_st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+// HAS_V / HAS_R: the call kind (matrix, residual, both) fixed per launch, so each body compiles lean.
+// ORD (FEM_SCATTER_TILED): every contribution is formed first; the visit then takes its turn (record
+// order, vseq) on each tile row it writes, adds with plain read-modify-writes and passes the turns on, so
+// each accumulator entry sums its contributions in a fixed order.  !ORD: shared-memory fp64 atomics.
+template <bool HAS_V, bool HAS_R, bool ORD = false>
 __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to, const P2Coef& H,
                                          const double* __restrict__ lt, double* sc, int v, unsigned char* sm) {
   const int lane = threadIdx.x & 31;
@@ -89,6 +103,15 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
     if (lane == 0)
       atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL),
                 (unsigned long long)reinterpret_cast<const int32_t*>(sm + to.velem)[v]);
+    if constexpr (ORD) {  // pass the turns on, or later visits of these rows would wait forever
+      const int16_t* ow = reinterpret_cast<const int16_t*>(sm + to.vown) + v * 10;
+      const uint8_t* sq = sm + to.vseq + v * 10;
+      int* turn = reinterpret_cast<int*>(sm + to.turn);
+      if (lane < 10 && ow[lane] >= 0) {
+        while (p2_ld_acquire(turn + ow[lane]) != sq[lane]) __nanosleep(32);
+        p2_st_release(turn + ow[lane], sq[lane] + 1);
+      }
+    }
     __syncwarp();
     return;
   }
@@ -135,6 +158,7 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
   }
   const double w = o[9];
   const int li0 = own[a0], li1 = own[a1];
+  double res0[3] = {0.0, 0.0, 0.0}, res1[3] = {0.0, 0.0, 0.0};
   if constexpr (HAS_R) {  // r_(a,i) = -Σ_γ w σ_ij G_aj, reduced over the 4 points (lanes c)
 #pragma unroll
     for (int i = 0; i < 3; i++) {
@@ -144,14 +168,16 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
         t0 = fma(o[10 + i * 3 + j], G0[j], t0);
         t1 = fma(o[10 + i * 3 + j], G1[j], t1);
       }
-      t0 = -sum4_t2(t0);
-      t1 = -sum4_t2(t1);
-      double* racc = reinterpret_cast<double*>(sm + to.racc);
-      if (c == 0 && li0 >= 0) atomicAdd(racc + i * to.T + li0, t0);
-      if (c == 0 && r < 2 && li1 >= 0) atomicAdd(racc + i * to.T + li1, t1);
+      res0[i] = -sum4_t2(t0);
+      res1[i] = -sum4_t2(t1);
+      if constexpr (!ORD) {
+        double* racc = reinterpret_cast<double*>(sm + to.racc);
+        if (c == 0 && li0 >= 0) atomicAdd(racc + i * to.T + li0, res0[i]);
+        if (c == 0 && r < 2 && li1 >= 0) atomicAdd(racc + i * to.T + li1, res1[i]);
+      }
     }
   }
-  if constexpr (!HAS_V) {
+  if constexpr (!HAS_V && !ORD) {
     __syncwarp();
     return;
   }
@@ -174,66 +200,110 @@ __device__ __forceinline__ void p2_visit(const TiledParams& P, const P2Offs& to,
         dmma884_t2(M[j][k], w * A[j], B[k]);
       }
   };
-  auto kval = [&](int i, int m, int t, double tr) {
-    return -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
-  };
-  // tile 1: rows a0, columns b = 2c + t
-  gram(G0, G0);
-  if (li0 >= 0) {
-    const int d = tdeg[li0], sr = acc_row_stride(3, d, P.nnz_s);
-    double* base = acc + toff[li0];
+  double K1[2][9], K2[9], K3[9];  // the lane's contributions: tile 1 (two blocks), tile 2, tile 3
+  if constexpr (HAS_V) {
+    gram(G0, G0);
 #pragma unroll
     for (int t = 0; t < 2; t++) {
       const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
-      double* rowb = base + vloc[a0 * 10 + 2 * c + t];
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
-        for (int m = 0; m < 3; m++) atomicAdd(rowb + i * sr + m * d, kval(i, m, t, tr));
+        for (int m = 0; m < 3; m++) K1[t][i * 3 + m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
     }
-  }
-  // tile 2: pair (a0, 8 + t); c < 2 writes block (a0, 8 + c), c >= 2 the transposed block (8 + c - 2, a0)
-  gram(G0, G1);
-  {
-    const int t = c & 1;
-    double Ms[3][3];
+    gram(G0, G1);
+    {
+      const int t = c & 1;
+      double Ms[3][3];
 #pragma unroll
-    for (int j = 0; j < 3; j++)
+      for (int j = 0; j < 3; j++)
 #pragma unroll
-      for (int k = 0; k < 3; k++) Ms[j][k] = t ? M[j][k][1] : M[j][k][0];
-    const bool tr_blk = c >= 2;
-    const int ra = tr_blk ? 8 + t : a0, cb = tr_blk ? a0 : 8 + t;
-    const int li = own[ra];
-    if (li >= 0) {
+        for (int k = 0; k < 3; k++) Ms[j][k] = t ? M[j][k][1] : M[j][k][0];
       const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
-      double* rowb = acc + toff[li] + vloc[ra * 10 + cb];
-      const int d = tdeg[li], sr = acc_row_stride(3, d, P.nnz_s);
 #pragma unroll
       for (int i = 0; i < 3; i++)
 #pragma unroll
-        for (int m = 0; m < 3; m++) {
-          const double kv = -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0));
-          atomicAdd(rowb + (tr_blk ? m * sr + i * d : i * sr + m * d), kv);
-        }
+        for (int m = 0; m < 3; m++) K2[i * 3 + m] = -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0));
+    }
+    gram(G1, G1);
+    {
+      const int t = c & 1;
+      double Ms[3][3];
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) Ms[j][k] = t ? M[j][k][1] : M[j][k][0];
+      const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int m = 0; m < 3; m++) K3[i * 3 + m] = -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0));
     }
   }
-  // tile 3: pair (8 + (a0 & 1), 8 + t): lanes a0 < 2, c < 2 write block (8 + a0, 8 + c)
-  gram(G1, G1);
-  if (r < 2 && c < 2 && li1 >= 0) {
-    const int t = c;
-    double Ms[3][3];
+  // ---- ordered: the turns of the rows this visit writes (rows a0 by lanes (a0, 0); rows 8, 9 by (0..1, 1))
+  int* turn = reinterpret_cast<int*>(sm + to.turn);
+  const uint8_t* sq = sm + to.vseq + v * 10;
+  const int trow = c == 0 ? li0 : ((c == 1 && r < 2) ? li1 : -1);
+  const int tturn = c == 0 ? sq[a0] : ((c == 1 && r < 2) ? sq[8 + r] : 0);
+  if constexpr (ORD) {
+    if (trow >= 0)
+      while (p2_ld_acquire(turn + trow) != tturn) __nanosleep(32);
+    __syncwarp();
+  }
+  auto add = [&](double* p, double x) {
+    if constexpr (ORD) *p += x;
+    else atomicAdd(p, x);
+  };
+  if constexpr (HAS_V) {
+    // tile 1: rows a0, columns b = 2c + t
+    if (li0 >= 0) {
+      const int d = tdeg[li0], sr = acc_row_stride(3, d, P.nnz_s);
+      double* base = acc + toff[li0];
 #pragma unroll
-    for (int j = 0; j < 3; j++)
+      for (int t = 0; t < 2; t++) {
+        double* rowb = base + vloc[a0 * 10 + 2 * c + t];
 #pragma unroll
-      for (int k = 0; k < 3; k++) Ms[j][k] = t ? M[j][k][1] : M[j][k][0];
-    const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
-    double* rowb = acc + toff[li1] + vloc[a1 * 10 + 8 + t];
-    const int d = tdeg[li1], sr = acc_row_stride(3, d, P.nnz_s);
+        for (int i = 0; i < 3; i++)
 #pragma unroll
-    for (int i = 0; i < 3; i++)
+          for (int m = 0; m < 3; m++) add(rowb + i * sr + m * d, K1[t][i * 3 + m]);
+      }
+    }
+    // tile 2: pair (a0, 8 + t); c < 2 writes block (a0, 8 + c), c >= 2 the transposed block (8 + c - 2, a0)
+    {
+      const int t = c & 1;
+      const bool tr_blk = c >= 2;
+      const int ra = tr_blk ? 8 + t : a0, cb = tr_blk ? a0 : 8 + t;
+      const int li = own[ra];
+      if (li >= 0) {
+        double* rowb = acc + toff[li] + vloc[ra * 10 + cb];
+        const int d = tdeg[li], sr = acc_row_stride(3, d, P.nnz_s);
 #pragma unroll
-      for (int m = 0; m < 3; m++)
-        atomicAdd(rowb + i * sr + m * d, -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0)));
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) add(rowb + (tr_blk ? m * sr + i * d : i * sr + m * d), K2[i * 3 + m]);
+      }
+    }
+    // tile 3: pair (8 + (a0 & 1), 8 + t): lanes a0 < 2, c < 2 write block (8 + a0, 8 + c)
+    if (r < 2 && c < 2 && li1 >= 0) {
+      double* rowb = acc + toff[li1] + vloc[a1 * 10 + 8 + c];
+      const int d = tdeg[li1], sr = acc_row_stride(3, d, P.nnz_s);
+#pragma unroll
+      for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int m = 0; m < 3; m++) add(rowb + i * sr + m * d, K3[i * 3 + m]);
+    }
+  }
+  if constexpr (HAS_R && ORD) {
+    double* racc = reinterpret_cast<double*>(sm + to.racc);
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      if (c == 0 && li0 >= 0) racc[i * to.T + li0] += res0[i];
+      if (c == 0 && r < 2 && li1 >= 0) racc[i * to.T + li1] += res1[i];
+    }
+  }
+  __syncwarp();
+  if constexpr (ORD) {
+    if (trow >= 0) p2_st_release(turn + trow, tturn + 1);
   }
   __syncwarp();
 }
@@ -250,6 +320,7 @@ __device__ __forceinline__ void p2_gather_halo(const TiledParams& P, const uint8
   cp_async_commit();
 }
 
+template <bool ORD>
 __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_constant__ TiledParams P) {
   using C = TileCfg<ET_TET, 2, 3, 2>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -260,8 +331,9 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
 #define P2RBUF(i) (smem + 128 + (size_t)(i) * P.rec_cap)
 #define P2HBUF(i) (reinterpret_cast<double*>(smem + 128 + 2 * (size_t)P.rec_cap) + (size_t)(i) * P.hcap)
   double* acc = P2HBUF(2);
+  int* turn = reinterpret_cast<int*>(acc + P.acc_cap);
   TileSmem F;
-  unsigned char* fp = reinterpret_cast<unsigned char*>(acc + P.acc_cap);
+  unsigned char* fp = reinterpret_cast<unsigned char*>(turn + P.turn_cap);
   F.qp = fp;
   fp += std::max((size_t)P.rec_bytes * P2_FACET_WARPS, (size_t)8 * P2_SCRATCH * C::WARPS);
   F.vid = reinterpret_cast<int32_t*>(fp);
@@ -336,19 +408,23 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
       to.tdeg = rb + L.o_tdeg; to.toff = rb + L.o_toff;
       to.acc = (uint32_t)(reinterpret_cast<unsigned char*>(acc) - smem);
       to.racc = to.acc + 8u * (uint32_t)acc_n;
+      to.vseq = rb + L.o_vseq;
+      to.turn = (uint32_t)(reinterpret_cast<unsigned char*>(turn) - smem);
       to.H = H;
       to.T = T;
     }
     for (int i = tid; i < acc_n + 3 * T; i += blockDim.x) acc[i] = 0.0;
+    if constexpr (ORD)
+      for (int i = tid; i < T; i += blockDim.x) turn[i] = 0;
     cp_async_wait_all();
     __syncthreads();
     double* wsc = reinterpret_cast<double*>(F.qp) + (size_t)P2_SCRATCH * warp;
     if (P.values && P.rhs)
-      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<true, true>(P, to, Hc, lanetab, wsc, v, smem);
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<true, true, ORD>(P, to, Hc, lanetab, wsc, v, smem);
     else if (P.values)
-      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<true, false>(P, to, Hc, lanetab, wsc, v, smem);
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<true, false, ORD>(P, to, Hc, lanetab, wsc, v, smem);
     else
-      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<false, true>(P, to, Hc, lanetab, wsc, v, smem);
+      for (int v = grab_visits(ctr, 1); v < nv; v = grab_visits(ctr, 1)) p2_visit<false, true, ORD>(P, to, Hc, lanetab, wsc, v, smem);
     if (next < P.n_tiles) {
       mbar_wait(&mbar[oth], (uint32_t)(((it + 1) >> 1) & 1));
       p2_gather_halo(P, P2RBUF(oth), P2HBUF(oth));
@@ -366,7 +442,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
     F.vloc = rec + L.o_vloc;
     F.hdat = P2HBUF(cur);
     F.H = H;
-    if (fmask) rec_facets<ET_TET, 2, 3, 2, P2_FACET_WARPS>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % P2_FACET_WARPS));
+    if (fmask) rec_facets<ET_TET, 2, 3, 2, P2_FACET_WARPS, ORD>(P, F, rec, L, F.qp + (size_t)P.rec_bytes * (warp % P2_FACET_WARPS));
     tile_epilogue<3>(P, F);
     __syncthreads();
   }
@@ -375,12 +451,18 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_p2_rec(const __grid_consta
 }
 
 // P2 tets, 4-point rule, domain terms all ELAST_DOMAIN.
-int launch_p2_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled) {
+int launch_p2_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_t s, bool* handled) {
   *handled = false;
   if (P.n_dom == 0 || !T.rec) return 0;
   for (int f = 0; f < P.n_dom; f++)
     if (P.dom[f].form != FEM_WF_ELAST_DOMAIN) return 0;
   *handled = true;
+  if (det && T.max_turns > 255) {
+    set_error("tiled scatter: a tile point is touched by more than 255 element visits (8-bit turns); use "
+              "FEM_SCATTER_COLOURED or FEM_SCATTER_TILED_UNORDERED");
+    return FEM_E_UNSUPPORTED;
+  }
+  P.turn_cap = (int)((T.max_tile_nodes + 3) / 4 * 4);
   using C = TileCfg<ET_TET, 2, 3, 2>;
   P.rec_bytes = (int)((sizeof(typename C::QPG) * C::NQF + 15) / 16 * 16);
   P.fvmax = 1;
@@ -395,18 +477,20 @@ int launch_p2_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool*
   P.acc_cap = (int)((P.values ? T.acc_max : 0) + (int64_t)3 * T.max_tile_nodes);
   P.acc_cap = (P.acc_cap + 1) / 2 * 2;
   const size_t fac_bytes = std::max((size_t)P.rec_bytes * P2_FACET_WARPS, (size_t)8 * P2_SCRATCH * C::WARPS) + 16;
-  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap + fac_bytes;
+  const size_t smem = 128 + 2 * (size_t)P.rec_cap + 2 * 8 * (size_t)P.hcap + 8 * (size_t)P.acc_cap +
+                      4 * (size_t)P.turn_cap + fac_bytes;
   if (smem + 4096 > 227 * 1024) {
     set_error("P2 record kernel: shared memory request too large (" + std::to_string(smem) + " B)");
     return FEM_E_UNSUPPORTED;
   }
-  FEM_CUDA_TRY(cudaFuncSetAttribute(k_p2_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = det ? k_p2_rec<true> : k_p2_rec<false>;
+  FEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (T.n_tiles <= 0) return 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(T.n_tiles, sms);
-  k_p2_rec<<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
+  kern<<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -767,9 +767,9 @@ int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_proble
     const int rc = launch_ns_tiled(P, T, det, s, &handled);
     if (handled) return rc;
   }
-  if (!det && et == ET_TET && o == 2 && kh == 3 && q == 2) {  // P2 elasticity: atomic-accumulating kernel
+  if (et == ET_TET && o == 2 && kh == 3 && q == 2) {  // P2 elasticity (c3)
     bool handled = false;
-    const int rc = launch_p2_tiled(P, T, s, &handled);
+    const int rc = launch_p2_tiled(P, T, det, s, &handled);
     if (handled) return rc;
   }
 #define FEM_GEN(ET_, ORD_, KH_) \

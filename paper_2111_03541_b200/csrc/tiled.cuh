@@ -649,6 +649,6 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cudaStream_t s, bool* handled);
 int launch_ns_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_t s, bool* handled);
-int launch_p2_tiled(TiledParams& P, const TileSchedule& T, cudaStream_t s, bool* handled);
+int launch_p2_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_t s, bool* handled);
 
 }  // namespace fem
