@@ -51,8 +51,85 @@ FLOPS_PER_ELEM = {"c5": 15456}
 DMMA_PEAK_TFLOPS = 36.0  # measured fp64 DMMA m8n8k4 peak (profiles/r01_m0b_dmma_smem.txt)
 
 # the record-driven kernel the tiled path launches per configuration (csrc/tiled.cu launch_tiled)
-TILED_KERNEL = {"c1": "k_tiled<TRI,P1>", "c2": "k_hex_rec<1,DET>", "c3": "k_p2_rec", "c4": "k_ns_rec",
-                "c5": "k_hex_rec<3,DET>"}
+TILED_KERNEL = {"c1": "k_gen_rec<TRI,P1,DET>", "c2": "k_hex_rec<1,DET>", "c3": "k_p2_rec<ORD>",
+                "c4": "k_ns_rec<DET> + coloured facet pass", "c5": "k_hex_sweep (z-sweep schedule)"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _oracle_worker(args):
+    name, steps = args
+    r = run_oracle_steps(name, steps, 0)
+    return r["elements"] * steps, r["s_per_step"] * steps
+
+
+def oracle_all_cores(name, seconds_per_core=8.0):
+    """The same serial oracle, unmodified, run as one process per host core on the bounded sample
+    (throughput of the CPU reference on the whole host: elements/s summed over the concurrent runs)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    one = run_oracle_steps(name, 1, 0)
+    steps = max(1, int(seconds_per_core / max(one["s_per_step"], 1e-6)))
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_oracle_worker, [(name, steps)] * cores)
+    wall = time.perf_counter() - t0
+    elems = sum(r[0] for r in res)
+    return {"value": elems / wall, "unit": "elements/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{cores} concurrent serial-oracle processes x {steps} step(s) on the {name} sub-box "
+                      f"({one['elements']} elements each), wall {wall:.1f} s"}
+
+
+def extra_entry(name, variant, scatter, steps, warmup):
+    """One keyed entry of the reported matrix: ms per step (matrix + residual), elements/s,
+    nnz/s and the HBM fraction of the algorithmic bytes, for another config / variant, same timing rules."""
+    import torch
+    from paper_2111_03541_b200 import FemSystem, fem
+    peaks, _ = _peaks()
+    mesh, prob = make_config(name, variant)
+    state = make_state(name, mesh, prob)
+    t0 = time.perf_counter()
+    S = FemSystem(mesh, prob)
+    torch.cuda.synchronize()
+    t_pat = time.perf_counter() - t0
+    S.alloc(True, True)
+    sd = torch.from_numpy(state).cuda()
+    out = {}
+    for sc in scatter:
+        def step():
+            fem.fem_assemble_system(S.mesh_h, S.pat_h, prob, sd, S.values, S.rhs, 0, sc, P=S.P)
+        for _ in range(warmup):
+            step()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / steps
+        ab = algorithmic_bytes(mesh, prob, S.nnz, S.kh * mesh.n_nodes)
+        out[sc] = {"ms_per_step": ms, "elements_per_s": mesh.n_elems / (ms * 1e-3), "nnz_per_s": S.nnz / (ms * 1e-3),
+                   "hbm_frac": ab / (ms * 1e-3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)),
+                   "kernel": TILED_KERNEL.get(name) if sc == "tiled" else f"{sc} path",
+                   "deterministic": sc in ("tiled", "coloured")}
+    status = S.status()
+    res = {"workload": f"{name}: {CONFIGS[name].desc}", "variant": variant, "elements": mesh.n_elems,
+           "nnz": S.nnz, "pattern_build_s": t_pat, "status": list(status), "by_scatter": out}
+    S.close()
+    del sd
+    torch.cuda.empty_cache()
+    return res
 
 
 def _traffic(name, variant, scatter):
@@ -181,6 +258,7 @@ def main():
     ap.add_argument("--scatter", default="tiled", choices=["tiled", "atomic", "coloured"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the keyed c2-c4 / perturbed-c5 entries")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -281,10 +359,12 @@ def main():
         alg_bytes = algorithmic_bytes(mesh, prob, nnz_total, S.kh * mesh.n_nodes)
         achieved = alg_bytes / (kern_ms * 1e-3) / 1e9 / world
         traffic, traffic_src = _traffic(name, args.variant, args.scatter) if world == 1 else (None, None)
-        cpu = None
+        cpu = cpu_all = None
         if not args.no_cpu_baseline and world == 1:
             r = run_oracle_steps(name, 1, 0)
-            cpu = {"value": r["value"], "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": r["sample"]}
+            cpu = {"value": r["value"], "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": r["sample"],
+                   "cpu_model": cpu_model()}
+            cpu_all = oracle_all_cores(name)
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": E_total / (ms * 1e-3), "unit": "elements/s", "n_gpus": world,
@@ -310,6 +390,7 @@ def main():
                      "frac": (FLOPS_PER_ELEM[name] * E_total / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS
                               if name in FLOPS_PER_ELEM else None)},
             "cpu_baseline": cpu,
+            "cpu_baseline_all_cores": cpu_all,
             "e2e": {"value": E_total / (e2e_ms * 1e-3), "unit": "elements/s",
                     "h2d_bytes_per_step": int(state.nbytes), "d2h_bytes_per_step": 16,
                     "ms_per_step": e2e_ms, "call": "fem_linearize_host_async (pipelined H2D)"},
@@ -317,8 +398,24 @@ def main():
             "clocks": clocks,
             "status": list(status),
         }
-        print(json.dumps(line), flush=True)
     S.close()
+    if rank == 0 and world == 1 and not args.no_extras and args.config == "c5":
+        # the rest of the reported matrix, measured in the same run (not the headline): c2-c4 structured
+        # and the perturbed-unstructured c5, TILED (deterministic) and for c3/c4 also TILED_UNORDERED
+        del sd
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        extras = {}
+        for nm, var, scs in [("c2", "structured", ["tiled"]), ("c3", "structured", ["tiled", "tiled_unordered"]),
+                             ("c4", "structured", ["tiled", "tiled_unordered"]), ("c5", "perturbed", ["tiled"])]:
+            try:
+                extras[f"{nm}/{var}"] = extra_entry(nm, var, scs, max(3, min(args.steps, 10)), 3)
+            except Exception as exc:  # reported, never hidden
+                extras[f"{nm}/{var}"] = {"error": repr(exc)}
+        line["extra"] = extras
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -281,6 +281,23 @@ int fem_bicgstab_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* col
  *   (no FMA contraction).  The Newton update φ ← φ − Δφ of D-4 and sign flips around the
  *   solves run here, not in the binding.  Stream-ordered, no sync.  INVALID_ARG on n < 0 / NULL. */
 int fem_vec_axpby(int64_t n, double alpha, const double* x, double beta, double* y, void* stream);
+/* fem_gmres_solve — restarted GMRES(restart) with right point-block-Jacobi preconditioning for K x = b with
+ *   a non-symmetric, indefinite K: the stabilised NS saddle point, where Jacobi-BiCGStab diverges.
+ *   The κ̂ x κ̂ diagonal block of every control point (rows κ·n_points + α of the κ-major numbering, B-3
+ *   P:368-375) is inverted once (Gauss-Jordan, partial pivoting); n_rows must equal n_points·kappa_hat
+ *   (single-GPU pattern, kappa_hat 1..4).  Arnoldi by classical Gram-Schmidt with re-orthogonalisation;
+ *   every inner product is a fixed-order reduction (bit-identical run to run); the host solves the small
+ *   Hessenberg problem and syncs once per Arnoldi step.  Stops when the true ||b - K x|| <= rtol·||b||
+ *   (within 10x of the recurrence's estimate) or after max_iter Arnoldi steps; x holds the initial guess on
+ *   entry.  pin_row >= 0: solve with that row and column replaced by the identity and the pinned unknown held
+ *   at its initial value (the gauge of a singular K: the paper's NS forms determine the pressure only up to a
+ *   constant, reading L29 — pin one pressure row, e.g. dim·n_points); -1: no pin.  work: caller-owned DEVICE
+ *   buffer of fem_gmres_work_doubles(n_rows, n_points, kappa_hat, restart) doubles.  Errors: INVALID_ARG (bad
+ *   sizes, singular point block), NAN (breakdown). */
+int64_t fem_gmres_work_doubles(int64_t n_rows, int64_t n_points, int kappa_hat, int restart);
+int fem_gmres_solve(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
+                    int64_t n_points, int kappa_hat, const double* b, double* x, int restart, int max_iter,
+                    double rtol, int64_t pin_row, double* work, int* iters_out, double* relres_out, void* stream);
 int fem_spmv(int64_t n_rows, const int64_t* rowptr, const int32_t* colidx, const double* values,
              const double* x, double* y, double alpha, double beta, void* stream);
 int64_t fem_cg_work_doubles(int64_t n_rows);

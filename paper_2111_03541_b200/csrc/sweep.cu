@@ -213,13 +213,18 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
         for (int64_t k = 0; k < nsteps; k++) {
           const int64_t l = layers[k];
           std::vector<int32_t>& V = layer_vis[k];
-          // visit order = turn order, colour-sorted: the visits of one colour share no row, so the visits the
-          // consumer warps take at the same time rarely wait for each other (measured: natural lattice order
-          // 2.6x slower, colours interleaved 1.7x)
-          std::stable_sort(V.begin(), V.end(), [&](int32_t a, int32_t b) { return m->h_colour[a] < m->h_colour[b]; });
+          // visit order = turn order, sorted by the lattice parity class (i mod 2, j mod 2) of the element: the
+          // four classes of a layer share no point, so the visits the consumer warps take at the same time
+          // rarely wait for each other (measured: natural lattice order 2.6x slower, classes interleaved
+          // 1.7x; the mesh's greedy colouring of a renumbered mesh has 17 colours and costs 1.45x)
+          auto cls = [&](int32_t e) {
+            const int32_t* bb = &lat[3 * (int64_t)conn[e]];
+            return (bb[0] & 1) + 2 * (bb[1] & 1);
+          };
+          std::stable_sort(V.begin(), V.end(), [&](int32_t a, int32_t b) { return cls(a) < cls(b); });
           std::vector<int32_t> run{0};
           for (size_t v = 1; v < V.size(); v++)
-            if (m->h_colour[V[v]] != m->h_colour[V[v - 1]]) run.push_back((int32_t)v);
+            if (cls(V[v]) != cls(V[v - 1])) run.push_back((int32_t)v);
           run.push_back((int32_t)V.size());
           // rows of planes l, l+1 (ring positions), zero / write lists
           std::vector<int16_t> zrow, wrow;

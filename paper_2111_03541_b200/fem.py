@@ -132,6 +132,10 @@ def lib():
         L.fem_pattern_csr.argtypes = [V, C.POINTER(V), C.POINTER(V), C.POINTER(I64)]
         L.fem_spmv.argtypes = [I64, V, V, V, V, V, C.c_double, C.c_double, V]
         L.fem_vec_axpby.argtypes = [I64, C.c_double, V, C.c_double, V, V]
+        L.fem_gmres_work_doubles.argtypes = [I64, I64, I, I]
+        L.fem_gmres_work_doubles.restype = I64
+        L.fem_gmres_solve.argtypes = [I64, V, V, V, I64, I, V, V, I, I, C.c_double, I64, V, C.POINTER(I),
+                                      C.POINTER(C.c_double), V]
         L.fem_cg_work_doubles.argtypes = [I64]
         L.fem_cg_work_doubles.restype = I64
         L.fem_cg_solve.argtypes = [I64, V, V, V, V, V, C.c_double, I, C.c_double, I, V, C.POINTER(I),
@@ -155,7 +159,8 @@ EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pa
             "fem_linearize_host", "fem_linearize_host_async", "fem_pattern_export_coo", "fem_gather", "fem_get_status", "fem_mesh_info", "fem_pattern_destroy",
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
             "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve",
-            "fem_time_init", "fem_time_effective", "fem_time_increment", "fem_vec_axpby"]
+            "fem_time_init", "fem_time_effective", "fem_time_increment", "fem_vec_axpby",
+            "fem_gmres_work_doubles", "fem_gmres_solve"]
 
 
 def _check(rc):
@@ -277,6 +282,21 @@ def fem_spmv(n_rows, rowptr, colidx, values, x, y, alpha=1.0, beta=0.0, stream=N
 def fem_vec_axpby(n, alpha, x, beta, y, stream=None):
     """y = alpha x + beta y on the device (fem_vec_axpby)."""
     _check(lib().fem_vec_axpby(int(n), float(alpha), _ptr(x), float(beta), _ptr(y), _stream(stream)))
+
+
+def fem_gmres_work_doubles(n_rows, n_points, kappa_hat, restart=30):
+    return int(lib().fem_gmres_work_doubles(int(n_rows), int(n_points), int(kappa_hat), int(restart)))
+
+
+def fem_gmres_solve(n_rows, rowptr, colidx, values, n_points, kappa_hat, b, x, work, restart=30, max_iter=2000,
+                    rtol=1e-10, pin_row=-1, stream=None):
+    """Point-block-Jacobi GMRES(restart) for K x = b (row/column pin_row pinned to the identity when >= 0);
+    returns (Arnoldi steps, ||b - K x|| / ||b|| of the pinned system)."""
+    it, rel = C.c_int(0), C.c_double(0.0)
+    _check(lib().fem_gmres_solve(int(n_rows), _ptr(rowptr), _ptr(colidx), _ptr(values), int(n_points),
+                                 int(kappa_hat), _ptr(b), _ptr(x), int(restart), int(max_iter), float(rtol),
+                                 int(pin_row), _ptr(work), C.byref(it), C.byref(rel), _stream(stream)))
+    return it.value, rel.value
 
 
 def fem_cg_work_doubles(n_rows):

@@ -91,10 +91,11 @@ class FemSystem:
         return self.values, self.rhs
 
     # ---- NEXT-1: the Newton sub-step's linear solve (D-4) on the GPU
-    def solve(self, b, x=None, spd_sign=-1.0, rtol=1e-12, max_iter=20000, check_every=16, method="cg"):
+    def solve(self, b, x=None, spd_sign=-1.0, rtol=1e-12, max_iter=20000, check_every=16, method="cg", restart=30):
         """Solve K x = b for the last assembled K (self.values).  method "cg": Jacobi-PCG on (spd_sign K)
         — the elasticity K is symmetric negative definite in the paper's sign convention (reading L17);
-        "bicgstab": Jacobi-BiCGStab for non-symmetric K (thermal FIX, NS).  Returns (x, iterations,
+        "bicgstab": Jacobi-BiCGStab for non-symmetric K (thermal FIX); "gmres": point-block-Jacobi GMRES(restart)
+        for the NS saddle point.  Returns (x, iterations,
         ||r|| / ||r0||).  Single-GPU patterns only."""
         if self.own != (0, self.N):
             raise ValueError("solve: the iterative solvers take a single-GPU (unpartitioned) pattern")
@@ -107,6 +108,14 @@ class FemSystem:
                                             device=self.device)
             it, rel = fem.fem_cg_solve(self.n_rows, rp, ci, self.values, b, x, self._cg_work, spd_sign, max_iter,
                                        rtol, check_every)
+        elif method == "gmres":
+            need = fem.fem_gmres_work_doubles(self.n_rows, self.N, self.kh, restart)
+            if getattr(self, "_gm_work", None) is None or self._gm_work.numel() < need:
+                self._gm_work = torch.empty(need, dtype=torch.float64, device=self.device)
+            # NS: pin the pressure of point 0 (the paper's forms fix the pressure only up to a constant, L29)
+            pin = self.dim * self.N if self.problem.physics == "ns" else -1
+            it, rel = fem.fem_gmres_solve(self.n_rows, rp, ci, self.values, self.N, self.kh, b, x, self._gm_work,
+                                          restart, max_iter, rtol, pin)
         elif method == "bicgstab":
             if getattr(self, "_bi_work", None) is None:
                 self._bi_work = torch.empty(fem.fem_bicgstab_work_doubles(self.n_rows), dtype=torch.float64,
@@ -125,20 +134,20 @@ class FemSystem:
         fem.fem_spmv(self.n_rows, rp, ci, self.values, x, y, alpha, beta)
         return y
 
-    def _solve_checked(self, d, method, spd_sign, rtol, max_iter):
+    def _solve_checked(self, d, method, spd_sign, rtol, max_iter, restart=200):
         """Solve K y = d (y = -Δφ of D-4) and reject a NaN / non-converged solve (returns y, it, rel)."""
-        y, it, rel = self.solve(d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method)
+        y, it, rel = self.solve(d, spd_sign=spd_sign, rtol=rtol, max_iter=max_iter, method=method, restart=restart)
         if not math.isfinite(rel):
             raise fem.FemError(-5, f"linear solve broke down (relative residual {rel})")
         return y, it, rel
 
-    def newton_step(self, state, scatter="tiled", spd_sign=-1.0, rtol=1e-12, max_iter=20000, method="cg"):
+    def newton_step(self, state, scatter="tiled", spd_sign=-1.0, rtol=1e-12, max_iter=20000, method="cg", restart=200):
         """One Newton sub-step (D-1..D-4) for a static problem: assemble K and d at φ, solve
         K Δφ = -d as K y = d, φ ← φ - y (fem_vec_axpby).  Returns the new state (level 0
         updated), the solver iterations and the relative residual ||r||/||r0|| (compare with rtol: hitting
         max_iter is reported, not raised; a NaN raises FemError)."""
         K, d = self.system(state, scatter=scatter)
-        y, it, rel = self._solve_checked(d, method, spd_sign, rtol, max_iter)
+        y, it, rel = self._solve_checked(d, method, spd_sign, rtol, max_iter, restart)
         new = state.clone()
         fem.fem_vec_axpby(self.kh * self.N, -1.0, y, 1.0, new[0])
         return new, it, rel

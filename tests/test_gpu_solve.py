@@ -33,11 +33,8 @@ def _csr(ora):
 
 
 @pytest.mark.parametrize("name,dims", [("c1", (8,)), ("c3", (7, 3, 2)), ("c4", (9, 4, 3)), ("c5", (7, 5, 6))])
-@pytest.mark.parametrize("spmv", ["row", "tma"])
-def test_spmv_matches_scipy_on_oracle_matrix(name, dims, spmv, monkeypatch):
+def test_spmv_matches_scipy_on_oracle_matrix(name, dims):
     _need_gpu()
-    if spmv == "tma":
-        monkeypatch.setenv("FEM_SPMV_TMA", "1")
     from paper_2111_03541_b200 import FemSystem
     m, p = make_config(name, "perturbed", dims)
     st = make_state(name, m, p)
@@ -57,11 +54,8 @@ def test_spmv_matches_scipy_on_oracle_matrix(name, dims, spmv, monkeypatch):
 
 
 @pytest.mark.parametrize("name,dims", [("c5", (7, 5, 6)), ("c3", (7, 3, 2))])
-@pytest.mark.parametrize("spmv", ["row", "tma"])
-def test_cg_matches_direct_solve_and_is_bit_reproducible(name, dims, spmv, monkeypatch):
+def test_cg_matches_direct_solve_and_is_bit_reproducible(name, dims):
     _need_gpu()
-    if spmv == "tma":  # the TMA-staged SpMV variant (read at launch)
-        monkeypatch.setenv("FEM_SPMV_TMA", "1")
     import scipy.sparse.linalg as spla
     from paper_2111_03541_b200 import FemSystem
     m, p = make_config(name, "perturbed", dims)
@@ -186,3 +180,55 @@ def test_gpu_manufactured_convergence_rate(etype, ns):
     errs = [_gpu_manufactured_error(n, etype) for n in ns]
     rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
     assert all(1.8 < r < 2.3 for r in rates), (errs, rates)
+
+
+@pytest.mark.parametrize("variant", ["structured", "perturbed"])
+def test_ns_newton_step_gmres_matches_direct_solve(variant):
+    """NEXT-1 remainder: the stabilised NS saddle point, where Jacobi-BiCGStab diverges, solved by
+    point-block-Jacobi GMRES on the GPU with the pressure of point 0 pinned (L29): the Newton increment of
+    small c4 matches scipy's direct solve of the ORACLE's pinned K and d within 10·κ·rtol, the solve is
+    bit-identical run to run, and a Newton sub-step through the ABI reduces ||d||."""
+    _need_gpu()
+    import scipy.sparse.linalg as spla
+    from paper_2111_03541_b200 import FemSystem
+    m, p = make_config("c4", variant, (9, 4, 3))
+    st = make_state("c4", m, p)
+    ora = oracle.assemble(m, p, st)
+    N = m.n_nodes
+    pin = 3 * N
+    K = _csr(ora).tolil()
+    K[pin, :] = 0.0
+    K[:, pin] = 0.0
+    K[pin, pin] = 1.0
+    K = K.tocsr()
+    b = -ora["rhs"].copy()
+    b[pin] = 0.0
+    x_ref = spla.spsolve(K.tocsc(), b)
+    S = FemSystem(m, p)
+    sd = torch.from_numpy(st).cuda()
+    S.system(sd, scatter="tiled")
+    d = S.rhs.clone()
+    rtol = 1e-11
+    x, it, rel = S.solve(-d, rtol=rtol, max_iter=5000, method="gmres", restart=200)
+    assert rel <= 10 * rtol and it > 0, (it, rel)
+    xn = x.cpu().numpy()
+    kappa = np.linalg.cond(K.toarray())
+    assert np.linalg.norm(xn - x_ref) / np.linalg.norm(x_ref) <= 10 * kappa * rtol
+    assert xn[pin] == 0.0
+    x2, it2, rel2 = S.solve(-d, rtol=rtol, max_iter=5000, method="gmres", restart=200)
+    assert it2 == it and rel2 == rel and torch.equal(x2, x)
+    # Newton consistency of the increment: d(φ + εΔ) = (1 - ε) d(φ) + O(ε²) on every row but the pinned one
+    dn = d.cpu().numpy()
+    mask = np.ones(len(dn), bool)
+    mask[pin] = False
+    errs = []
+    for eps in (1e-3, 2e-3):
+        st_e = sd.clone()
+        st_e[0] += eps * x.view(4, N)
+        S.system(st_e, scatter="tiled")
+        errs.append(np.linalg.norm((S.rhs.cpu().numpy() - (1 - eps) * dn)[mask]))
+    assert errs[1] / errs[0] == pytest.approx(4.0, rel=0.1), errs
+    # and a full Newton sub-step runs through the ABI with the pinned GMRES (φ ← φ + Δφ in the library)
+    st1, it1, rel1 = S.newton_step(sd, scatter="tiled", rtol=1e-10, max_iter=5000, method="gmres")
+    assert rel1 <= 1e-9 and float(st1[0, 3, 0]) == float(sd[0, 3, 0])  # pinned pressure unchanged
+    S.close()

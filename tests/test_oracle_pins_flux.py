@@ -22,6 +22,7 @@ import numpy as np
 import pytest
 
 import oracle
+from fem_inputs import make_config as make_config_, make_state as make_state_
 from fem_inputs.meshgen import facets_on_plane, hex_box, tet_box, tri_square
 from helpers import problem
 
@@ -320,3 +321,18 @@ def test_ns_inflow_profile_converges_to_closed_form():
     assert errs[-1].max() < 2e-3, errs
     rates = np.log2(errs[:-1] / errs[1:])
     assert rates[1:].min() >= 2.5, (errs, rates)
+
+
+def test_ns_jacobian_has_the_constant_pressure_null_vector():
+    """Reading L29 (pinned on the oracle): with NS_boundary_BASE on every boundary group a constant
+    pressure drops out of every row: K·[0; 1] = 0 to rounding, so the Newton system needs a pressure gauge."""
+    m, p = make_config_("c4", "perturbed", (6, 3, 3))
+    st = make_state_("c4", m, p)
+    ora = oracle.assemble(m, p, st)
+    import scipy.sparse as sp
+    n = len(ora["rowptr"]) - 1
+    K = sp.csr_matrix((ora["values"], ora["colidx"], ora["rowptr"]), shape=(n, n))
+    N = m.n_nodes
+    e = np.zeros(4 * N)
+    e[3 * N:] = 1.0
+    assert np.abs(K @ e).max() <= 1e-10 * abs(K).max()
