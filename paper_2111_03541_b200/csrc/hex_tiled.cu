@@ -997,6 +997,9 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
   uint64_t* empty = full + SW_NBUF;                     // [SW_NBUF]
   uint64_t* landed = empty + SW_NBUF;                   // [SW_NBUF] record bulk copies
   __shared__ double lanetab[32 * LANE_TAB];
+  __shared__ TileOffs tofs[SW_NBUF];  // per ring buffer: the step's section offsets (written by the producer)
+  __shared__ uint32_t tvfm[SW_NBUF];
+  __shared__ int tnv[SW_NBUF];
   auto rbuf = [&](int b) { return smem + 128 + (size_t)b * P.rec_cap; };
   auto hbuf = [&](int b) { return reinterpret_cast<double*>(smem + 128 + (size_t)SW_NBUF * P.rec_cap) + (size_t)b * P.hcap; };
   double* acc = hbuf(SW_NBUF);
@@ -1026,7 +1029,7 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
   }
   if (tid == 0) {
     for (int b = 0; b < SW_NBUF; b++) {
-      mbar_init(&full[b], 32);             // the producer's 32 lanes (cp.async arrive.noinc)
+      mbar_init(&full[b], 33);             // the producer's 32 lanes (cp.async arrive.noinc) + its offsets
       mbar_init(&empty[b], SW_CONSUMERS);  // one arrive per consumer warp
       mbar_init(&landed[b], 1);
     }
@@ -1064,6 +1067,24 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
         const double* base = c < 3 ? P.coords + (int64_t)c * P.N : P.state + (int64_t)(c - 3) * P.N;
         for (int i = lane; i < H; i += 32) cp_async8(hb + c * H + i, base + hn[i]);
       }
+      if (lane == 0) {  // the step's offsets for the consumers (released by the arrive below)
+        TileOffs o;
+        const uint32_t rb = (uint32_t)(rec - smem);
+        const int acc_n = P.values ? hdr[4] : 0;
+        o.vown = rb + L.o_vown; o.vhal = rb + L.o_vhal; o.velem = rb + L.o_velem; o.vloc = rb + L.o_vloc;
+        o.hdat = (uint32_t)(reinterpret_cast<const unsigned char*>(hb) - smem);
+        o.tdeg = rb + L.o_tdeg; o.toff = rb + L.o_toff; o.tnode = rb + L.o_tnode; o.trps = rb + L.o_trps;
+        o.acc = (uint32_t)(reinterpret_cast<unsigned char*>(acc) - smem);
+        o.racc = o.acc + 8u * (uint32_t)acc_n;
+        o.vseq = rb + L.o_vsw;
+        o.turn = (uint32_t)(reinterpret_cast<unsigned char*>(turn) - smem);
+        o.H = H;
+        o.T = hdr[0];
+        tofs[b] = o;
+        tvfm[b] = rb + L.o_vfm;
+        tnv[b] = hdr[2];
+        mbar_arrive(&full[b]);
+      }
       cp_async_mbar_arrive_noinc(&full[b]);
       t = next_of(t, q);
     }
@@ -1076,23 +1097,9 @@ __global__ void __launch_bounds__(HEX_THREADS, 1) k_hex_sweep(const __grid_const
     const int b = (int)(k % SW_NBUF);
     mbar_wait_sleep(&full[b], (uint32_t)(k / SW_NBUF) & 1u);
     mbar_wait(&landed[b], (uint32_t)(k / SW_NBUF) & 1u);  // (already complete) the record's bulk copy is visible
-    const uint8_t* rec = rbuf(b);
-    const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
-    const RecLayout L = rec_layout_hdr(8, hdr);
-    const int nv = hdr[2];
-    const int acc_n = P.values ? hdr[4] : 0;
-    TileOffs to;
-    const uint32_t rb = (uint32_t)(rec - smem);
-    to.vown = rb + L.o_vown; to.vhal = rb + L.o_vhal; to.velem = rb + L.o_velem; to.vloc = rb + L.o_vloc;
-    to.hdat = (uint32_t)(reinterpret_cast<const unsigned char*>(hbuf(b)) - smem);
-    to.tdeg = rb + L.o_tdeg; to.toff = rb + L.o_toff; to.tnode = rb + L.o_tnode; to.trps = rb + L.o_trps;
-    to.acc = (uint32_t)(reinterpret_cast<unsigned char*>(acc) - smem);
-    to.racc = to.acc + 8u * (uint32_t)acc_n;
-    to.vseq = rb + L.o_vsw;
-    to.turn = (uint32_t)(reinterpret_cast<unsigned char*>(turn) - smem);
-    to.H = hdr[1];
-    to.T = hdr[0];
-    const uint32_t* vfm = reinterpret_cast<const uint32_t*>(rec + L.o_vfm);
+    const TileOffs to = tofs[b];
+    const int nv = tnv[b];
+    const uint32_t* vfm = reinterpret_cast<const uint32_t*>(smem + tvfm[b]);
     // visits round-robin over the consumers, continuing the rotation of the previous step (49 visits on 15
     // warps would otherwise always give warps 0-3 the extra visit and let them fall steps behind)
     for (int v = (warp - rot + SW_CONSUMERS) % SW_CONSUMERS; v < nv; v += SW_CONSUMERS)
