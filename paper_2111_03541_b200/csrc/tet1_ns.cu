@@ -22,8 +22,20 @@ struct NsCoef {
   double rho, mu, tm, tc, f0;
 };
 
-// Per-visit point data in the warp scratch (doubles): G[4][3] | gu[4][3] | Rc | w | u[4 points][4] | Rm[4][3]
-constexpr int NS_SC = 12 + 12 + 2 + 16 + 12;  // 54 doubles per visit
+// Per-visit data in the warp scratch (doubles): G[4][3] | gu[4][3] | Rc | w | u[4 points][4] | Rm[4][3] at
+// 0..53, then the quadrature moments of the visit (offsets NSM_*): every point-dependent factor of the
+// NS tangent and residual is linear in the point (affine P1: N_b(γ), u(γ), Rm(γ) = ρ u_k(γ) u_i,k
+// + p_,i), so the 4-point sums of the 16 pair blocks collapse to contractions of these 49 moments with the
+// constant gradients (the sums are hoisted out of the pair loop; the quadrature itself is kept,
+// so the result is the oracle's 4-point sum, not the exact integral).
+constexpr int NSM_U1 = 54;   // U1[b][i] = Σ_γ w N_b(γ) u_i(γ)          (4 x 3)
+constexpr int NSM_R1 = 66;   // R1[b][i] = Σ_γ w N_b(γ) Rm_i(γ)         (4 x 3)
+constexpr int NSM_UU = 78;   // UU[i][j] = Σ_γ w u_i(γ) u_j(γ)          (3 x 3)
+constexpr int NSM_UR = 87;   // UR[j][i] = Σ_γ w u_j(γ) Rm_i(γ)         (3 x 3)
+constexpr int NSM_U0 = 96;   // U0[i] = Σ_γ w u_i(γ)                      (3)
+constexpr int NSM_R0 = 99;   // R0[i] = Σ_γ w Rm_i(γ)                     (3)
+constexpr int NSM_P0 = 102;  // P0 = Σ_γ w p(γ)                           (1)
+constexpr int NS_SC = 104;   // doubles per visit (even)
 
 template <bool DET>
 __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& D, const NsCoef& c, int v0, int nv,
@@ -112,6 +124,49 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
       const double* u = sc + 26 + q * 4;
       sc[42 + q * 3 + i] = sc[12 + 9 + i] + c.rho * (u[0] * sc[12 + i * 3 + 0] + u[1] * sc[12 + i * 3 + 1] + u[2] * sc[12 + i * 3 + 2]);
     }
+    __syncwarp();
+    // ---- phase 1b: the visit's quadrature moments (lanes of the half split them)
+    {
+      const double wq = sc[25];
+      if (l16 < 12) {  // U1[b][i], R1[b][i] for (b, i) = (l16 / 3, l16 % 3)
+        const int bb = l16 / 3, i = l16 % 3;
+        double u1 = 0.0, r1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const double wn = wq * (q == bb ? be : al);
+          u1 = fma(wn, sc[26 + q * 4 + i], u1);
+          r1 = fma(wn, sc[42 + q * 3 + i], r1);
+        }
+        sc[NSM_U1 + l16] = u1;
+        sc[NSM_R1 + l16] = r1;
+      }
+      if (l16 < 9) {  // UU[i][j], UR[i][j] = Σ w u_i Rm_j for (i, j) = (l16 / 3, l16 % 3)
+        const int i = l16 / 3, j = l16 % 3;
+        double uu = 0.0, ur = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          uu = fma(wq * sc[26 + q * 4 + i], sc[26 + q * 4 + j], uu);
+          ur = fma(wq * sc[26 + q * 4 + i], sc[42 + q * 3 + j], ur);
+        }
+        sc[NSM_UU + l16] = uu;
+        sc[NSM_UR + l16] = ur;
+      } else if (l16 < 12) {  // U0[i], R0[i]
+        const int i = l16 - 9;
+        double u0 = 0.0, r0 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          u0 = fma(wq, sc[26 + q * 4 + i], u0);
+          r0 = fma(wq, sc[42 + q * 3 + i], r0);
+        }
+        sc[NSM_U0 + i] = u0;
+        sc[NSM_R0 + i] = r0;
+      } else if (l16 == 12) {  // P0
+        double p0 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) p0 = fma(wq, sc[26 + q * 4 + 3], p0);
+        sc[NSM_P0] = p0;
+      }
+    }
   }
   if (__any_sync(0xffffffffu, bad)) {
     if (bad) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)D.vid[v]);
@@ -143,45 +198,48 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
   for (int k = 0; k < 3; k++) GaGb = fma(Ga[k], Gb[k], GaGb);
 #pragma unroll
   for (int m = 0; m < 3; m++) smv[m] = Ga[0] * sc[12 + 0 * 3 + m] + Ga[1] * sc[12 + 1 * 3 + m] + Ga[2] * sc[12 + 2 * 3 + m];
+  // ---- the 4x4 pair block and the residual row as contractions of the moments (phase 1b)
+  const double W = 4.0 * w, Wq = w;  // Σ_γ w = |T|;  Σ_γ w N_b(γ) = w (β + 3α = 1)
+  const double* U1b = sc + NSM_U1 + b * 3;
+  const double* R1b = sc + NSM_R1 + b * 3;
+  const double* UU = sc + NSM_UU;
+  const double* UR = sc + NSM_UR;
+  const double* U0 = sc + NSM_U0;
+  double s1 = 0.0, s2 = 0.0, aU0 = 0.0, bU0 = 0.0;  // G_a·U1_b, G_a^T UU G_b, G_a·U0, U0·G_b
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    s1 = fma(Ga[k], U1b[k], s1);
+    aU0 = fma(Ga[k], U0[k], aU0);
+    bU0 = fma(Gb[k], U0[k], bU0);
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; j++) t = fma(UU[k * 3 + j], Gb[j], t);
+    s2 = fma(Ga[k], t, s2);
+  }
   double acc[4][4];
+  const double diag = -rho * s1 + mu * W * GaGb + tm * rho * rho * s2;
 #pragma unroll
-  for (int i = 0; i < 4; i++)
+  for (int i = 0; i < 3; i++) {
 #pragma unroll
-    for (int m = 0; m < 4; m++) acc[i][m] = 0.0;
-  double res = 0.0;
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const double* u = sc + 26 + q * 4;
-    const double* Rm = sc + 42 + q * 3;
-    const double Na = (a == q) ? be : al, Nb = (b == q) ? be : al;
-    const double Aa = Ga[0] * u[0] + Ga[1] * u[1] + Ga[2] * u[2];
-    const double Bb = Gb[0] * u[0] + Gb[1] * u[1] + Gb[2] * u[2];
-    const double wNb = w * Nb;
-    const double diag = w * (-rho * Nb * Aa + mu * GaGb + tm * rho * rho * Aa * Bb);
-    const double c_uu = w * tm * rho * rho * Aa * Nb;
-    const double c_rm = tm * rho * wNb;
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-      const double ui = u[i], Rmi = Rm[i];
-#pragma unroll
-      for (int m = 0; m < 3; m++) {
-        double t = Ga[m] * (c_rm * Rmi - rho * wNb * ui) + c_uu * sc[12 + i * 3 + m] + tc * w * Ga[i] * Gb[m];
-        if (i == m) t += diag;
-        acc[i][m] += t;
-      }
-      acc[i][3] += w * (-Ga[i] * Nb + tm * rho * Aa * Gb[i]);
-      acc[3][i] += w * (Na * Gb[i] + tm * rho * (Nb * smv[i] + Ga[i] * Bb));
+    for (int m = 0; m < 3; m++) {
+      double t = Ga[m] * (tm * rho * R1b[i] - rho * U1b[i]) + tm * rho * rho * s1 * sc[12 + i * 3 + m] +
+                 tc * W * Ga[i] * Gb[m];
+      if (i == m) t += diag;
+      acc[i][m] = t;
     }
-    acc[3][3] += w * tm * GaGb;
-    if (b < 3) {  // residual row (a, u_b): BASE + SUPG of NS_domain
-      const int i = b;
-      double r = -Ga[i] * u[3] + tc * Ga[i] * Rc + tm * rho * Aa * Rm[i];
+    acc[i][3] = -Ga[i] * Wq + tm * rho * Gb[i] * aU0;
+    acc[3][i] = Wq * Gb[i] + tm * rho * (Wq * smv[i] + Ga[i] * bU0);
+  }
+  acc[3][3] = tm * W * GaGb;
+  double res;
+  if (b < 3) {  // residual row (a, u_b): BASE + SUPG of NS_domain
+    const int i = b;
+    res = -Ga[i] * sc[NSM_P0] + tc * W * Ga[i] * Rc;
 #pragma unroll
-      for (int j = 0; j < 3; j++) r += Ga[j] * (mu * sc[12 + i * 3 + j] - rho * u[i] * u[j]);
-      res += w * r;
-    } else {       // residual row (a, p)
-      res += w * (Na * Rc + tm * (Ga[0] * Rm[0] + Ga[1] * Rm[1] + Ga[2] * Rm[2]));
-    }
+    for (int j = 0; j < 3; j++)
+      res += Ga[j] * (tm * rho * UR[j * 3 + i] + mu * W * sc[12 + i * 3 + j] - rho * UU[i * 3 + j]);
+  } else {      // residual row (a, p)
+    res = Wq * Rc + tm * (Ga[0] * sc[NSM_R0] + Ga[1] * sc[NSM_R0 + 1] + Ga[2] * sc[NSM_R0 + 2]);
   }
   if constexpr (DET) {
     // ordered: visit v takes its turn (vseq) on the accumulator row of each owned node, so every entry
