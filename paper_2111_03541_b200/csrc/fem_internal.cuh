@@ -195,6 +195,8 @@ struct AsmArgs {
 };
 
 int launch_generic(const AsmArgs& A, bool facet);
+// quadratic-cube elasticity domain term on the fp64 tensor cores (hex2_el.cu); *handled = 0: not applicable
+int launch_q2_elast(const AsmArgs& A, int* handled);
 // z-sweep schedule for Q1-hex elasticity on lattice meshes (sweep.cu); FEM_E_UNSUPPORTED: not applicable
 int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s);
 int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_problem* prob,

@@ -413,16 +413,25 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
     const TaskList& L = (T.region < 0) ? m->dom : m->bnd[T.region];
     A.task_elem = L.elem;
     A.task_facet = (T.region < 0) ? nullptr : L.facet;
+    // element kernel: quadratic-cube elasticity on the fp64 tensor cores, else the generic batch kernel
+    auto launch_el = [&](const AsmArgs& a) {
+      if (T.region < 0) {
+        int handled = 0;
+        const int r = launch_q2_elast(a, &handled);
+        if (handled) return r;
+      }
+      return launch_generic(a, T.region >= 0);
+    };
     if (scatter == FEM_SCATTER_ATOMIC) {
       A.task_begin = 0; A.task_count = L.n;
       if (T.region < 0) A.task_elem = nullptr;  // natural element order
-      rc = launch_generic(A, T.region >= 0);
+      rc = launch_el(A);
       if (rc) return rc;
     } else {
       for (size_t c = 0; c + 1 < L.col_off.size(); c++) {
         A.task_begin = L.col_off[c];
         A.task_count = L.col_off[c + 1] - L.col_off[c];
-        rc = launch_generic(A, T.region >= 0);
+        rc = launch_el(A);
         if (rc) return rc;
       }
     }
