@@ -81,11 +81,18 @@ extern "C" {
  *                        by more than 255 visits.
  * FEM_SCATTER_TILED_UNORDERED  owner gather with shared-memory fp64 atomics where a kernel has them (P2 and
  *                        NS tets, generic tiles; hex as TILED): faster, summation order varies run to run.
- *                        Residual-only calls on tetrahedra use the atomic element pass. */
+ *                        Residual-only calls on tetrahedra use the atomic element pass.
+ * FEM_SCATTER_STORED     element-stored gather (D-2/D-3 split over HBM): every element writes its whole local
+ *                        block and residual into a scratch owned by the pattern, then every CSR entry sums the
+ *                        blocks of the elements that contain its two points in ELEMENT ORDER and every row its
+ *                        elements' residual rows: no atomics, bit-identical run to run, complete rows written
+ *                        (accumulate must be 0).  Needs fem_pattern_stored_prepare first (FEM_E_INVALID_ARG
+ *                        otherwise).  Every element type and physics. */
 #define FEM_SCATTER_ATOMIC 0
 #define FEM_SCATTER_COLOURED 1
 #define FEM_SCATTER_TILED 2
 #define FEM_SCATTER_TILED_UNORDERED 3
+#define FEM_SCATTER_STORED 4
 
 #define FEM_TIME_STATIC 0
 #define FEM_TIME_GENALPHA 1
@@ -264,6 +271,13 @@ int fem_pattern_info(fem_pattern_t pat, int64_t* out9);
  *   A zero p·Kp or r·z freezes the iterate instead of dividing by zero.  Not converging within max_iter
  *   is NOT an error: check relres_out against rtol.  Errors: FEM_E_INVALID_ARG for bad arguments or a
  *   non-positive diagonal of s K (not SPD); FEM_E_NAN when the residual becomes NaN. */
+/* fem_pattern_stored_prepare — one-time setup of FEM_SCATTER_STORED for this pattern: the per-slot
+ *   contribution lists (a stable device radix sort of the slot map: 4 B per (element, a, b) with an owned
+ *   row), the diagonal slot of every owned row, and the element scratch — residual rows E·n_loc·κ̂ doubles,
+ *   and with with_matrix != 0 the element blocks E·n_loc²·κ̂² doubles (c3: 5.3 GB).  Library-owned, freed by
+ *   fem_pattern_destroy; a second call only adds what is missing.  Synchronizes `stream`.  Errors:
+ *   FEM_E_INDEX_OVERFLOW when E·n_loc² >= 2^32, FEM_E_OOM, FEM_E_CUDA. */
+int fem_pattern_stored_prepare(fem_pattern_t pat, int with_matrix, void* stream);
 /* fem_pattern_csr — the pattern's own DEVICE CSR arrays (library-owned, valid until fem_pattern_destroy,
  *   read-only): rowptr int64 [n_rows+1], colidx int32 [nnz] (global column ids; *col_offset = own_lo, 0
  *   on a single GPU).  No copy, no sync. */

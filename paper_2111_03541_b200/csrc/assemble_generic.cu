@@ -18,6 +18,8 @@ int launch_generic(const AsmArgs& A, bool facet) {
   P.rowptr_s = A.pat ? A.pat->rowptr_s : nullptr;
   P.plain = A.plain;
   P.err = m->err;
+  P.ek = A.ek; P.er = A.er; P.ek_add = A.ek_add; P.ek_nb = A.pat ? A.pat->st_nb : 0;
+  P.ek_map = A.ek_map;
   const int et = m->etype, o = m->order;
   if (et == ET_TRI && o == 1) return gen_dispatch_tri(m->kh, A.quad_order, P, A.stream, facet);
   if (et == ET_HEX && o == 1) return gen_dispatch_hex(m->kh, A.quad_order, P, A.stream, facet);

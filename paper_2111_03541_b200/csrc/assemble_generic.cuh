@@ -75,6 +75,11 @@ struct GenParams {
   const int64_t* rowptr_s;
   int plain;
   long long* err;
+  double* ek = nullptr;  // FEM_SCATTER_STORED: element blocks [E][ek_nb][st_bs(KH)] (values unused)
+  int ek_nb = 0;
+  double* er = nullptr;  // FEM_SCATTER_STORED: element residuals [E][NL][KH] (rhs unused)
+  int ek_add = 0;        // 0: store (first domain term), 1: add
+  const int32_t* ek_map = nullptr;  // storage index of element e (null: e); < 0: not stored
 };
 
 template <int ET, int ORD, int KH, int Q, bool FACET>
@@ -254,10 +259,22 @@ __global__ void __launch_bounds__(128) k_generic(const GenParams P) {
       const int64_t task = base + be;
       if (task >= P.task_count || bad[be]) continue;
       const int node = nodes[be * NL + a];
-      if (node < P.own_lo || node >= P.own_hi) continue;
+      // stored mode: every row of the element (a symmetric block (a, b), a <= b, serves the owned row b even
+      // when row a belongs to another part)
+      const bool owned = node >= P.own_lo && node < P.own_hi;
+      if (!owned && !P.ek && !P.er) continue;
       const int64_t li = node - P.own_lo;
       const QPt* qe = qs + be * NQ;
-      if (P.rhs) {
+      const int64_t ti = P.task_begin + task;
+      const int64_t e = P.task_elem ? P.task_elem[ti] : ti;
+      const int64_t es = P.ek_map ? (int64_t)P.ek_map[e] : e;  // element storage index (stored mode)
+      if (P.er) {  // FEM_SCATTER_STORED: the element's own residual rows (stored, or added by later terms)
+        double r = 0.0;
+#pragma unroll
+        for (int g = 0; g < NQ; g++) r += qe[g].w * form_res<DIM, NL, KH>(P.F, qe[g], a, k0);
+        double* dst = P.er + (es * NL + a) * KH + k0;
+        *dst = (P.ek_add ? *dst : 0.0) + r;
+      } else if (P.rhs && owned) {
         double r = 0.0;
 #pragma unroll
         for (int g = 0; g < NQ; g++) r += qe[g].w * form_res<DIM, NL, KH>(P.F, qe[g], a, k0);
@@ -265,9 +282,22 @@ __global__ void __launch_bounds__(128) k_generic(const GenParams P) {
         if (P.plain) *dst += r;
         else atomicAdd(dst, r);
       }
-      if (P.values && P.F.form != FEM_WF_ELAST_LOAD) {
-        const int64_t ti = P.task_begin + task;
-        const int64_t e = P.task_elem ? P.task_elem[ti] : ti;
+      if (P.ek && P.F.form != FEM_WF_ELAST_LOAD) {  // FEM_SCATTER_STORED: block (a, b) of the element
+        // symmetric physics (ek_nb = NL(NL+1)/2): the blocks b >= a only, packed row by row
+        const bool sym = P.ek_nb != NL * NL;
+        const int64_t eb = es * P.ek_nb;
+        for (int b = sym ? a : 0; b < NL; b++) {
+          const int blk = sym ? a * NL - a * (a - 1) / 2 + (b - a) : a * NL + b;
+          double* dst = P.ek + (eb + blk) * (KH == 1 ? 1 : (KH * KH + 3) / 4 * 4) + k0 * KH;  // stride st_bs(KH)
+#pragma unroll
+          for (int kl = 0; kl < KH; kl++) {
+            double v = 0.0;
+#pragma unroll
+            for (int g = 0; g < NQ; g++) v += qe[g].w * form_tan<DIM, NL, KH>(P.F, qe[g], a, k0, b, kl);
+            dst[kl] = (P.ek_add ? dst[kl] : 0.0) + v;
+          }
+        }
+      } else if (P.values && P.F.form != FEM_WF_ELAST_LOAD && owned) {
         const int64_t rps = P.rowptr_s[li];
         const int64_t deg = P.rowptr_s[li + 1] - rps;
         const int64_t rowbase = (int64_t)k0 * KH * P.nnz_s + (int64_t)KH * rps;

@@ -174,6 +174,33 @@ struct fem_pattern_s {
   int32_t* colidx = nullptr;    // device [nnz]
   int tiles_rc = 0;             // != 0: no tile schedule for this mesh (tiled calls return it)
   std::string tiles_msg;
+  // FEM_SCATTER_STORED (stored.cu, fem_pattern_stored_prepare).  Elements are stored in the Morton order of
+  // their centroids (position pos, eperm[pos] = e, epos[e] = pos).  Per scalar slot s its contributions
+  // (pos, a, b) at ent[off[s] .. off[s+1]), encoded (pos·NB + blk) << 1 | transposed; per owned row its
+  // residual contributions pos·NL + a at rent[roff[li] .. roff[li+1]).
+  uint32_t* st_ent = nullptr;
+  uint32_t* st_off = nullptr;
+  uint32_t* st_rent = nullptr;
+  uint32_t* st_roff = nullptr;
+  int32_t* st_epos = nullptr;
+  int32_t* st_eperm = nullptr;
+  int32_t* st_rows = nullptr;  // owned rows in gather order (row items of the flow schedule)
+  double* st_ek = nullptr;     // [E][NB][KH][KH] (only with with_matrix)
+  double* st_er = nullptr;     // [E][NL][KH]
+  int64_t st_n_ent = 0;
+  int st_nb = 0;               // blocks stored per element: NL(NL+1)/2 (symmetric physics, a <= b) or NL²
+  // flow schedule (fused element + gather kernels, stored.cuh)
+  int32_t* st_sched = nullptr;
+  int32_t* st_dep = nullptr;
+  uint32_t* st_done = nullptr;
+  uint32_t* st_ticket = nullptr;
+  int64_t st_n_items = 0, st_n_ei = 0;
+  int st_ei = 0, st_ri = 0;
+  // boundary terms of the flow path: element -> compact index, and their blocks / residual rows
+  int32_t* st_bmap = nullptr;
+  double* st_fk = nullptr;
+  double* st_fr = nullptr;
+  int64_t st_n_bnd = 0;
 };
 
 namespace fem {
@@ -192,9 +219,17 @@ struct AsmArgs {
   const int8_t* task_facet;  // null for domain terms
   int64_t task_begin, task_count;
   cudaStream_t stream;
+  double* ek = nullptr;  // FEM_SCATTER_STORED element blocks / residuals (stored.cu); values/rhs unused then
+  double* er = nullptr;
+  int ek_add = 0;
+  const int32_t* ek_map = nullptr;  // element -> storage index (null: identity)
 };
 
 int launch_generic(const AsmArgs& A, bool facet);
+// FEM_SCATTER_STORED: element pass into the pattern's element scratch, then the per-slot gathers (stored.cu)
+int launch_stored(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem* prob, const double* state,
+                  double* values, double* rhs, cudaStream_t s);
+void stored_free(fem_pattern_s* p);
 // quadratic-cube elasticity domain term on the fp64 tensor cores (hex2_el.cu); *handled = 0: not applicable
 int launch_q2_elast(const AsmArgs& A, int* handled);
 // z-sweep schedule for Q1-hex elasticity on lattice meshes (sweep.cu); FEM_E_UNSUPPORTED: not applicable

@@ -235,7 +235,7 @@ static int run_q2_kind(const GenParams& P, cudaStream_t s) {
 int launch_q2_elast(const AsmArgs& A, int* handled) {
   *handled = 0;
   const fem_mesh_s* m = A.m;
-  if (m->order != 2 || (m->etype != ET_HEX && m->etype != ET_HEXS) || m->kh != 3 ||
+  if (A.ek || A.er || m->order != 2 || (m->etype != ET_HEX && m->etype != ET_HEXS) || m->kh != 3 ||
       A.F.form != FEM_WF_ELAST_DOMAIN || (A.quad_order != 2 && A.quad_order != 3))
     return 0;
   *handled = 1;

@@ -259,6 +259,7 @@ int fem_mesh_info(fem_mesh_t m, int* n_loc, int* kappa_hat, int* n_colours, int6
 void fem_pattern_destroy(fem_pattern_t p) {
   if (!p) return;
   tiles_free(p->tiles);
+  stored_free(p);
   cudaFree(p->rowptr_s); cudaFree(p->colidx_s); cudaFree(p->slot); cudaFree(p->rowptr); cudaFree(p->colidx);
   delete p;
 }
@@ -362,6 +363,11 @@ static int assemble(fem_mesh_t m, fem_pattern_t p, const fem_problem* prob, cons
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   bool bnd_only = false;  // tiled NS: domain terms in the tile kernel, boundary terms coloured afterwards
+  if (scatter == FEM_SCATTER_STORED) {
+    if (accumulate) { set_error("stored scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
+    if (!p) { set_error("stored scatter needs the pattern"); return FEM_E_INVALID_ARG; }
+    return launch_stored(m, p, prob, state, values, rhs, s);
+  }
   const bool tiled = scatter == FEM_SCATTER_TILED || scatter == FEM_SCATTER_TILED_UNORDERED;
   if (tiled && accumulate) { set_error("tiled scatter writes complete rows; accumulate must be 0"); return FEM_E_INVALID_ARG; }
   if (tiled && !values && m->etype == FEM_TET) {

@@ -15,6 +15,7 @@
 #include <string>
 
 #include "tiled.cuh"
+#include "stored.cuh"
 
 namespace fem {
 
@@ -493,6 +494,291 @@ int launch_p2_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_
   kern<<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+
+// ---- FEM_SCATTER_STORED, fused element + gather kernel (stored.cu / stored.cuh flow_loop).  Element items:
+// one warp per element, the visit arithmetic above with the element's points gathered straight from HBM
+// (the warp's next element's node ids and coordinates load while the current one computes), the upper
+// blocks a <= b of the symmetric 10 x 10 block matrix K^e (55 of 100: tile 1 where b >= a, tile 2 without
+// its transposes, tile 3 where b >= a) and the residual rows staged in shared memory, the element's
+// boundary-term blocks added, and stored contiguously at its Morton position: ek[pos][blk][i][m],
+// er[pos][a][i].  Row items: the per-slot gathers of stored.cuh.
+constexpr int P2E_WARPS = 8;
+__device__ __forceinline__ int p2_ublk(int a, int b) { return a * 10 - a * (a - 1) / 2 + (b - a); }
+
+template <bool HAS_V, bool HAS_R>
+__global__ void __launch_bounds__(32 * P2E_WARPS) k_p2_flow(const double* __restrict__ coords, const double* __restrict__ state,
+                                                           const int32_t* __restrict__ conn, int64_t N, P2Coef H,
+                                                           long long* err, const FlowParams F) {
+  const int64_t E = F.E;
+  double* __restrict__ ek = F.ek;
+  double* __restrict__ er = F.er;
+  __shared__ double lanetab[32 * P2_LANE_TAB];
+  __shared__ double scr[P2E_WARPS][P2_SCRATCH];
+  // per-warp staging of the element's 55 blocks (+ 30 residual rows): the lanes' scattered 72-byte blocks
+  // leave as one contiguous, coalesced 3960-byte store stream per element
+  __shared__ double stage[P2E_WARPS][55 * 9 + 30];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {  // per-lane constants, as in k_p2_rec
+    using EL = Elem<ET_TET, 2>;
+    double* Lt = lanetab + tid;
+    for (int s = 0; s < 3; s++)
+      for (int t = 0; t < 2; t++) {
+        const int k = 4 * s + (tid & 3), n = 8 * t + (tid >> 2);
+        double val = 0.0;
+        if (k < 10 && n < 12) {
+          double xi[3], wq, Nn[10], dN[10][3];
+          EL::vol_qp(2, n / 3, xi, wq);
+          EL::shape(xi, Nn, dN);
+          val = dN[k][n % 3];
+        }
+        Lt[32 * (s * 2 + t)] = val;
+      }
+    double xi[3], wq, Nn[10], dN[10][3];
+    EL::vol_qp(2, tid & 3, xi, wq);
+    EL::shape(xi, Nn, dN);
+    const int a0 = tid >> 2, a1 = 8 + (a0 & 1);
+    for (int i = 0; i < 3; i++) {
+      Lt[32 * (6 + i)] = dN[a0][i];
+      Lt[32 * (9 + i)] = dN[a1][i];
+    }
+  }
+  __syncthreads();
+  const int c = lane & 3, r = lane >> 2;
+  const double* L = lanetab + lane;
+  double* sc = scr[warp];
+  // A fragments of the geometry GEMM for element e: component r (x, y, z, d1, d2, d3) of node 4s + c
+  auto load_av = [&](int64_t e, double (&av)[3]) {
+    const int nd = (lane < 10 && e >= 0) ? __ldg(conn + (int64_t)lane * E + e) : 0;
+#pragma unroll
+    for (int s = 0; s < 3; s++) {
+      const int k = 4 * s + c;
+      const int node = __shfl_sync(0xffffffffu, nd, k < 10 ? k : 0);
+      av[s] = 0.0;
+      if (k < 10 && e >= 0) {
+        if (r < 3) av[s] = __ldg(coords + (int64_t)r * N + node);
+        else if (HAS_R && r < 6) av[s] = __ldg(state + (int64_t)(r - 3) * N + node);
+      }
+    }
+  };
+  const uint64_t keep = st_policy_evict_last();
+  auto elem_item = [&](int item) {
+  const int64_t p0 = (int64_t)item * F.ei, p1 = p0 + F.ei < E ? p0 + F.ei : E;
+  int64_t pos = p0;
+  double av[3];
+  load_av(pos < p1 ? (int64_t)__ldg(F.eperm + pos) : -1, av);
+  for (; pos < p1; pos++) {
+    const int64_t e = __ldg(F.eperm + pos);
+    const int64_t pn = pos + 1;
+    double C2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int s = 0; s < 3; s++)
+#pragma unroll
+      for (int t = 0; t < 2; t++) dmma884_t2(C2[t], av[s], L[32 * (s * 2 + t)]);
+    load_av(pn < p1 ? (int64_t)__ldg(F.eperm + pn) : -1, av);  // prefetch: in flight while this element computes
+    if (r < 6) {
+#pragma unroll
+      for (int t = 0; t < 2; t++)
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+          const int n = 8 * t + 2 * c + i;
+          if (n < 12) sc[r * 12 + n] = C2[t][i];
+        }
+    }
+    __syncwarp();
+    const int q = lane >> 3;
+    double J[3][3], Dr[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        J[i][j] = sc[i * 12 + 3 * q + j];
+        if constexpr (HAS_R) Dr[i][j] = sc[(3 + i) * 12 + 3 * q + j];
+      }
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    if (__any_sync(0xffffffffu, !(det > 0.0))) {
+      if (lane == 0) atomicCAS((unsigned long long*)err, (unsigned long long)(-1LL), (unsigned long long)e);
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    if ((lane & 7) == 0) {
+      const double rr = 1.0 / det;
+      double Ji[3][3];
+      Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+      double* o = sc + q * 20;
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
+      const double w = det * (1.0 / 24.0);
+      o[9] = w;
+      if constexpr (HAS_R) {
+        double gu[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; k++)
+#pragma unroll
+          for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+        const double lw = H.sl * w * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * w;
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+      }
+    }
+    __syncwarp();
+    const int a0 = r;
+    const double* o = sc + c * 20;
+    double G0[3], G1[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      G0[i] = o[0 * 3 + i] * L[32 * 6] + o[1 * 3 + i] * L[32 * 7] + o[2 * 3 + i] * L[32 * 8];
+      G1[i] = o[0 * 3 + i] * L[32 * 9] + o[1 * 3 + i] * L[32 * 10] + o[2 * 3 + i] * L[32 * 11];
+    }
+    const double w = o[9];
+    if constexpr (HAS_R) {  // r_(a,i) = -Σ_γ w σ_ij G_aj over the 4 points (lanes c)
+      double res0[3], res1[3];
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          t0 = fma(o[10 + i * 3 + j], G0[j], t0);
+          t1 = fma(o[10 + i * 3 + j], G1[j], t1);
+        }
+        res0[i] = -sum4_t2(t0);
+        res1[i] = -sum4_t2(t1);
+      }
+      double* eo = stage[warp] + 55 * 9;
+      if (c == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; i++) eo[a0 * 3 + i] = res0[i];
+      }
+      if (c == 1 && r < 2) {
+#pragma unroll
+        for (int i = 0; i < 3; i++) eo[(8 + r) * 3 + i] = res1[i];
+      }
+    }
+    if constexpr (HAS_V) {
+      double M[3][3][2];
+      auto gram = [&](const double* A, const double* B) {
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+#pragma unroll
+          for (int k = 0; k < 3; k++) {
+            M[j][k][0] = 0.0;
+            M[j][k][1] = 0.0;
+            dmma884_t2(M[j][k], w * A[j], B[k]);
+          }
+      };
+      double* eb = stage[warp];
+      // tile 1: blocks (a0, 2c + t), upper ones only
+      gram(G0, G0);
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const int b = 2 * c + t;
+        if (b >= a0) {
+          const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+          double* dst = eb + p2_ublk(a0, b) * 9;
+#pragma unroll
+          for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int m = 0; m < 3; m++) dst[i * 3 + m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+        }
+      }
+      // tile 2: block (a0, 8 + c) for c < 2 (always upper)
+      gram(G0, G1);
+      if (c < 2) {
+        double Ms[3][3];
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+#pragma unroll
+          for (int k = 0; k < 3; k++) Ms[j][k] = c ? M[j][k][1] : M[j][k][0];
+        const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
+        double* dst = eb + p2_ublk(a0, 8 + c) * 9;
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) dst[i * 3 + m] = -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0));
+      }
+      // tile 3: blocks (8 + a0, 8 + c) for a0 <= c < 2
+      gram(G1, G1);
+      if (r < 2 && c < 2 && c >= r) {
+        double Ms[3][3];
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+#pragma unroll
+          for (int k = 0; k < 3; k++) Ms[j][k] = c ? M[j][k][1] : M[j][k][0];
+        const double tr = Ms[0][0] + Ms[1][1] + Ms[2][2];
+        double* dst = eb + p2_ublk(8 + r, 8 + c) * 9;
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int m = 0; m < 3; m++) dst[i * 3 + m] = -(H.cl * Ms[i][m] + H.cm * Ms[m][i] + (i == m ? H.cm * tr : 0.0));
+      }
+    }
+    __syncwarp();
+    const int bi = F.bmap ? __ldg(F.bmap + e) : -1;  // the element's boundary-term blocks, if any
+    if constexpr (HAS_V) {  // 55 blocks of 12 doubles (9 + pad): 256-bit stores, 3 per block
+      double* dst = ek + pos * (55 * 12);
+      const double* fb = bi >= 0 ? F.fk + (int64_t)bi * (55 * 12) : nullptr;
+      for (int g = lane; g < 55 * 3; g += 32) {
+        const int blk = g / 3, q = g - 3 * blk;
+        const double* sv = stage[warp] + blk * 9 + 4 * q;
+        double v[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) v[i] = (q < 2 || i == 0) ? sv[i] : 0.0;
+        if (fb) {
+#pragma unroll
+          for (int i = 0; i < 4; i++) v[i] += __ldg(fb + 12 * blk + 4 * q + i);
+        }
+        st_st4(dst + 12 * blk + 4 * q, v[0], v[1], v[2], v[3]);
+      }
+    }
+    if constexpr (HAS_R) {
+      const double* fb = bi >= 0 ? F.fr + (int64_t)bi * 30 : nullptr;
+      if (lane < 30) st_store_keep(er + pos * 30 + lane, fb ? stage[warp][55 * 9 + lane] + __ldg(fb + lane) : stage[warp][55 * 9 + lane], keep);
+    }
+    __syncwarp();  // the scratch and the stage are rewritten by the next element
+  }
+  };
+  flow_loop<3>(F, elem_item);
+}
+
+// P2 tets, 4-point rule, every domain term ELAST_DOMAIN (stored.cu checks): the fused stored-mode kernel.
+int launch_p2_flow(const fem_mesh_s* m, const fem_problem* prob, const FlowParams& F, const double* state,
+                   cudaStream_t s) {
+  P2Coef H = {0, 0, 0, 0};
+  for (int t = 0; t < prob->n_terms; t++) {
+    const fem_term& T = prob->terms[t];
+    if (T.region >= 0) continue;
+    const FormArgs Fa = make_form_args(prob, T);
+    H.cl += Fa.f0 * Fa.lam; H.cm += Fa.f0 * Fa.mu; H.sl += Fa.lam; H.sm += Fa.mu;
+  }
+  if (F.n_items == 0) return 0;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto go = [&](auto kern) -> int {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * P2E_WARPS, 0);
+    const int64_t grid = std::min<int64_t>(F.n_items, (int64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, 32 * P2E_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, H, m->err, F);
+    FEM_CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  if (F.ek && F.er) return go(k_p2_flow<true, true>);
+  if (F.ek) return go(k_p2_flow<true, false>);
+  return go(k_p2_flow<false, true>);
 }
 
 }  // namespace fem

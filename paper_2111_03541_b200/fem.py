@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("FEM_LIB_PATH") or os.path.join(_HERE, "libfem.so")  #
 
 FEM_TRI, FEM_TET, FEM_HEX, FEM_HEX_SERENDIPITY = 1, 2, 4, 5
 FEM_THERMAL, FEM_ELASTICITY, FEM_NS = 1, 2, 3
-SCATTER = {"atomic": 0, "coloured": 1, "tiled": 2, "tiled_unordered": 3}
+SCATTER = {"atomic": 0, "coloured": 1, "tiled": 2, "tiled_unordered": 3, "stored": 4}
 ETYPE = {"tri": FEM_TRI, "tet": FEM_TET, "hex": FEM_HEX, "hexs": FEM_HEX_SERENDIPITY}
 PHYSICS = {"thermal": FEM_THERMAL, "elasticity": FEM_ELASTICITY, "ns": FEM_NS}
 FORM = {
@@ -115,6 +115,7 @@ def lib():
         L.fem_pattern_nnz_s.restype = I64
         L.fem_pattern_export.argtypes = [V, V, V, V, V, V, V]
         L.fem_pattern_info.argtypes = [V, V]
+        L.fem_pattern_stored_prepare.argtypes = [V, I, V]
         L.fem_assemble_matrix.argtypes = [V, V, PP, V, V, I, I, V]
         L.fem_assemble_residual.argtypes = [V, V, PP, V, V, I, I, V]
         L.fem_assemble_system.argtypes = [V, V, PP, V, V, V, I, I, V]
@@ -160,7 +161,7 @@ EXPORTED = ["fem_mesh_create", "fem_pattern_build", "fem_pattern_nnz_s", "fem_pa
             "fem_mesh_destroy", "fem_last_error", "fem_version", "fem_pattern_csr", "fem_spmv",
             "fem_cg_work_doubles", "fem_cg_solve", "fem_bicgstab_work_doubles", "fem_bicgstab_solve",
             "fem_time_init", "fem_time_effective", "fem_time_increment", "fem_vec_axpby",
-            "fem_gmres_work_doubles", "fem_gmres_solve"]
+            "fem_gmres_work_doubles", "fem_gmres_solve", "fem_pattern_stored_prepare"]
 
 
 def _check(rc):
@@ -230,6 +231,10 @@ def fem_pattern_info(pat_h):
     keys = ["tiles", "max_tile_points", "max_acc_doubles", "max_record_bytes", "max_halo_points", "visits",
             "max_tile_visits", "record_bytes", "schedule"]
     return dict(zip(keys, out.tolist()))
+
+
+def fem_pattern_stored_prepare(pat_h, with_matrix=True, stream=None):
+    _check(lib().fem_pattern_stored_prepare(pat_h, int(bool(with_matrix)), _stream(stream)))
 
 
 def fem_pattern_export(pat_h, rowptr=None, colidx=None, slot_s=None, rowptr_s=None, colidx_s=None, stream=None):

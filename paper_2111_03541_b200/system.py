@@ -36,6 +36,7 @@ class FemSystem:
             self.nnz_s = fem.fem_pattern_nnz_s(self.pat_h)
         self.values = None
         self.rhs = None
+        self._stored = 0  # FEM_SCATTER_STORED setup: 0 none, 1 residual scratch, 2 with the element blocks
 
     def info(self):
         d = fem.fem_mesh_info(self.mesh_h)
@@ -72,19 +73,28 @@ class FemSystem:
             fem.fem_gather(self.nnz, out["csr_index"], self.values, out["values"])
         return out
 
+    def _prepare(self, scatter, matrix):
+        """FEM_SCATTER_STORED needs its one-time setup (contribution lists, element scratch) first."""
+        if scatter == "stored" and self._stored < (2 if matrix else 1):
+            fem.fem_pattern_stored_prepare(self.pat_h, with_matrix=matrix)
+            self._stored = 2 if matrix else 1
+
     def matrix(self, state, scatter="atomic", accumulate=False):
+        self._prepare(scatter, True)
         self.alloc(True, False)
         fem.fem_assemble_matrix(self.mesh_h, self.pat_h, self.problem, state, self.values, int(accumulate),
                                 scatter)
         return self.values
 
     def residual(self, state, scatter="atomic", accumulate=False):
+        self._prepare(scatter, False)
         self.alloc(False, True)
         fem.fem_assemble_residual(self.mesh_h, self.pat_h, self.problem, state, self.rhs, int(accumulate),
                                   scatter)
         return self.rhs
 
     def system(self, state, scatter="atomic", accumulate=False):
+        self._prepare(scatter, True)
         self.alloc(True, True)
         fem.fem_assemble_system(self.mesh_h, self.pat_h, self.problem, state, self.values, self.rhs,
                                 int(accumulate), scatter, P=self.P)

@@ -39,7 +39,7 @@ def _to_dev(st):
     return torch.from_numpy(st).cuda()
 
 
-SCATTERS = os.environ.get("FEM_SCATTERS", "atomic,coloured,tiled").split(",")
+SCATTERS = os.environ.get("FEM_SCATTERS", "atomic,coloured,tiled,stored").split(",")
 
 
 @pytest.mark.parametrize("name", list(SMALL))
@@ -74,10 +74,11 @@ def test_small_parity_all_modes(name, variant):
     S.close()
 
 
-@pytest.mark.parametrize("name,sc", [(n, sc) for n in ("c1", "c2", "c3", "c4", "c5") for sc in ("coloured", "tiled")])
+@pytest.mark.parametrize("name,sc", [(n, sc) for n in ("c1", "c2", "c3", "c4", "c5") for sc in ("coloured", "tiled", "stored")])
 def test_deterministic_modes_bit_exact(name, sc):
-    """FEM_SCATTER_COLOURED and FEM_SCATTER_TILED are deterministic by contract (libfem.h) on every element
-    type: hex (sweep / ordered tiles), P1 NS tets (ordered turns), P2 tets and triangles (colour runs).
+    """FEM_SCATTER_COLOURED, FEM_SCATTER_TILED and FEM_SCATTER_STORED are deterministic by contract (libfem.h)
+    on every element type: hex (sweep / ordered tiles), P1 NS tets (ordered turns), P2 tets (ordered turns),
+    triangles (colour runs); stored: element-order sums per CSR entry.
     Matrix, residual and the system call are bit-identical call after call."""
     _need_gpu()
     m, p = make_config(name, "perturbed", SMALL[name])

@@ -20,7 +20,7 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def _check(m, p, st, scatters=("atomic", "coloured")):
+def _check(m, p, st, scatters=("atomic", "coloured", "stored")):
     from helpers import poisoned_system
     ora = oracle.assemble(m, p, st, slot=True)
     assert ora["status"] == 0
