@@ -435,7 +435,8 @@ int launch_stored(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem
     F.ek = ek; F.er = er; F.values = values; F.rhs = rhs;
     return launch_p2_flow(m, prob, F, state, s);
   }
-  // ---- element pass: domain terms store (the first) or add into the scratch at the element's position
+  // ---- two-phase path: element pass (domain terms store (the first) or add into the scratch at the
+  // element's position), boundary terms added, then the gather kernel
   bool first = true;
   for (int t = 0; t < prob->n_terms && first; t++) {
     if (prob->terms[t].region >= 0) continue;

@@ -765,13 +765,13 @@ int launch_p2_flow(const fem_mesh_s* m, const fem_problem* prob, const FlowParam
     const FormArgs Fa = make_form_args(prob, T);
     H.cl += Fa.f0 * Fa.lam; H.cm += Fa.f0 * Fa.mu; H.sl += Fa.lam; H.sm += Fa.mu;
   }
-  if (F.n_items == 0) return 0;
+  if (F.n_items == 0 || F.n_ei == 0) return 0;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   auto go = [&](auto kern) -> int {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * P2E_WARPS, 0);
-    const int64_t grid = std::min<int64_t>(F.n_items, (int64_t)sms * std::max(per_sm, 1));
+    const int64_t grid = std::min<int64_t>((F.n_items + P2E_WARPS - 1) / P2E_WARPS, (int64_t)sms * std::max(per_sm, 1));
     kern<<<(unsigned)grid, 32 * P2E_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, H, m->err, F);
     FEM_CUDA_TRY(cudaGetLastError());
     return 0;
