@@ -106,6 +106,8 @@ def extra_entry(name, variant, scatter, steps, warmup):
     sd = torch.from_numpy(state).cuda()
     out = {}
     for sc in scatter:
+        if sc == "stored":  # one-time setup of FEM_SCATTER_STORED (contribution lists, element scratch)
+            fem.fem_pattern_stored_prepare(S.pat_h, with_matrix=True)
         def step():
             fem.fem_assemble_system(S.mesh_h, S.pat_h, prob, sd, S.values, S.rhs, 0, sc, P=S.P)
         for _ in range(warmup):
@@ -121,8 +123,10 @@ def extra_entry(name, variant, scatter, steps, warmup):
         ab = algorithmic_bytes(mesh, prob, S.nnz, S.kh * mesh.n_nodes)
         out[sc] = {"ms_per_step": ms, "elements_per_s": mesh.n_elems / (ms * 1e-3), "nnz_per_s": S.nnz / (ms * 1e-3),
                    "hbm_frac": ab / (ms * 1e-3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)),
-                   "kernel": TILED_KERNEL.get(name) if sc == "tiled" else f"{sc} path",
-                   "deterministic": sc in ("tiled", "coloured")}
+                   "kernel": (TILED_KERNEL.get(name) if sc == "tiled" else
+                              "k_p2_el + k_st_gather (element-stored, per-slot gather)" if sc == "stored" and name == "c3" else
+                              f"{sc} path"),
+                   "deterministic": sc in ("tiled", "coloured", "stored")}
     status = S.status()
     res = {"workload": f"{name}: {CONFIGS[name].desc}", "variant": variant, "elements": mesh.n_elems,
            "nnz": S.nnz, "pattern_build_s": t_pat, "status": list(status), "by_scatter": out}
@@ -401,13 +405,14 @@ def main():
     S.close()
     if rank == 0 and world == 1 and not args.no_extras and args.config == "c5":
         # the rest of the reported matrix, measured in the same run (not the headline): c2-c4 structured
-        # and the perturbed-unstructured c5, TILED (deterministic) and for c3/c4 also TILED_UNORDERED
+        # and the perturbed-unstructured c5, TILED (deterministic) and for c3/c4 also TILED_UNORDERED; c3 also
+        # STORED (deterministic element-stored gather, its fastest deterministic mode)
         del sd
         import gc
         gc.collect()
         torch.cuda.empty_cache()
         extras = {}
-        for nm, var, scs in [("c2", "structured", ["tiled"]), ("c3", "structured", ["tiled", "tiled_unordered"]),
+        for nm, var, scs in [("c2", "structured", ["tiled"]), ("c3", "structured", ["tiled", "tiled_unordered", "stored"]),
                              ("c4", "structured", ["tiled", "tiled_unordered"]), ("c5", "perturbed", ["tiled"])]:
             try:
                 extras[f"{nm}/{var}"] = extra_entry(nm, var, scs, max(3, min(args.steps, 10)), 3)

@@ -13,6 +13,7 @@
 
 #include "elements.cuh"
 #include "fem_internal.cuh"
+#include "stored.cuh"
 
 namespace fem {
 
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(128) k_generic(const GenParams P) {
         const int64_t eb = es * P.ek_nb;
         for (int b = sym ? a : 0; b < NL; b++) {
           const int blk = sym ? a * NL - a * (a - 1) / 2 + (b - a) : a * NL + b;
-          double* dst = P.ek + (eb + blk) * (KH == 1 ? 1 : (KH * KH + 3) / 4 * 4) + k0 * KH;  // stride st_bs(KH)
+          double* dst = P.ek + (eb + blk) * st_bs(KH) + k0 * KH;
 #pragma unroll
           for (int kl = 0; kl < KH; kl++) {
             double v = 0.0;

@@ -184,23 +184,11 @@ struct fem_pattern_s {
   uint32_t* st_roff = nullptr;
   int32_t* st_epos = nullptr;
   int32_t* st_eperm = nullptr;
-  int32_t* st_rows = nullptr;  // owned rows in gather order (row items of the flow schedule)
+  int32_t* st_rows = nullptr;  // owned rows in gather order (Morton order of their points)
   double* st_ek = nullptr;     // [E][NB][KH][KH] (only with with_matrix)
   double* st_er = nullptr;     // [E][NL][KH]
   int64_t st_n_ent = 0;
   int st_nb = 0;               // blocks stored per element: NL(NL+1)/2 (symmetric physics, a <= b) or NL²
-  // flow schedule (fused element + gather kernels, stored.cuh)
-  int32_t* st_sched = nullptr;
-  int32_t* st_dep = nullptr;
-  uint32_t* st_done = nullptr;
-  uint32_t* st_ticket = nullptr;
-  int64_t st_n_items = 0, st_n_ei = 0;
-  int st_ei = 0, st_ri = 0;
-  // boundary terms of the flow path: element -> compact index, and their blocks / residual rows
-  int32_t* st_bmap = nullptr;
-  double* st_fk = nullptr;
-  double* st_fr = nullptr;
-  int64_t st_n_bnd = 0;
 };
 
 namespace fem {

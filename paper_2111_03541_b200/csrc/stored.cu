@@ -2,17 +2,16 @@
 //
 // D-2 / D-3 add every element's local residual and local stiffness block into d and K.  The
 // paper increments a COO array atomically; the owner-gather tiles of tiled.cu sum inside shared memory.
-// This mode splits the sum into two halves joined through a scratch:
+// This mode splits the sum into two halves joined through a scratch in HBM:
 //   element  every element computes its whole local block K^e_(a,κ),(b,λ) (symmetric physics: the blocks
 //            a <= b) and residual d^e_(a,κ) and stores them at its position in the Morton order of element
-//            centroids — no conflicts, each element owns its storage;
+//            centroids — no conflicts, each element owns its storage (P2-tet elasticity: k_p2_el on the
+//            tensor cores, tet2_el.cu; everything else: the generic element kernel); boundary terms add
+//            into the owning element's storage;
 //   gather   every scalar CSR slot s = (row point, column point) sums the blocks of the elements that
 //            contain both points, in a fixed list order (built once by a stable radix sort of the slot map),
 //            and writes its κ̂² values; every owned row sums its elements' residual rows.
 // No atomics and a fixed summation order: bit-identical run to run, complete rows written.
-// Element types with a fused kernel (P2-tet elasticity, tet2_el.cu) run both halves in one persistent
-// dataflow launch so that the blocks are read back from L2 (stored.cuh); the others run the generic element
-// kernel into the scratch, then the gather kernel.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -106,38 +105,25 @@ __global__ void __launch_bounds__(256) k_st_gather(const int64_t* __restrict__ r
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_own; w += nw) {
     const int64_t li = __ldg(rows + w);
-    if (values) st_gather_row<KH, false>(li, rowptr_s, nnz_s, off, ent, ek, values);
-    if (rhs) st_res_row<KH, false>(li, n_own, roff, rent, er, rhs);
+    if (values) st_gather_row<KH>(li, rowptr_s, nnz_s, off, ent, ek, values);
+    if (rhs) st_res_row<KH>(li, n_own, roff, rent, er, rhs);
   }
 }
 
 void stored_free(fem_pattern_s* p) {
-  void* ptrs[] = {p->st_ent, p->st_off, p->st_rent, p->st_roff, p->st_epos, p->st_eperm, p->st_rows, p->st_ek,
-                  p->st_er, p->st_sched, p->st_dep, p->st_done, p->st_ticket, p->st_bmap, p->st_fk, p->st_fr};
+  void* ptrs[] = {p->st_ent, p->st_off, p->st_rent, p->st_roff, p->st_epos, p->st_eperm, p->st_rows, p->st_ek, p->st_er};
   for (void* q : ptrs) cudaFree(q);
   p->st_ent = p->st_off = p->st_rent = p->st_roff = nullptr;
-  p->st_epos = p->st_eperm = p->st_rows = p->st_sched = p->st_dep = p->st_bmap = nullptr;
-  p->st_ek = p->st_er = p->st_fk = p->st_fr = nullptr;
-  p->st_done = p->st_ticket = nullptr;
-  p->st_n_ent = p->st_n_items = p->st_n_ei = p->st_n_bnd = 0;
-  p->st_nb = p->st_ei = p->st_ri = 0;
+  p->st_epos = p->st_eperm = p->st_rows = nullptr;
+  p->st_ek = p->st_er = nullptr;
+  p->st_n_ent = 0;
+  p->st_nb = 0;
 }
 
-// fused element + gather kernel of P2-tet elasticity (tet2_el.cu)
-int launch_p2_flow(const fem_mesh_s* m, const fem_problem* prob, const FlowParams& F, const double* state,
-                   cudaStream_t s);
-// problems with a flow kernel: P2-tet elasticity, 4-point rule, every domain term ELAST_DOMAIN
-static bool flow_ok(const fem_mesh_s* m, const fem_problem* prob) {
-  if (!(m->etype == FEM_TET && m->order == 2 && m->kh == 3 && m->physics == FEM_ELASTICITY && prob->quad_order == 2))
-    return false;
-  int n_dom = 0;
-  for (int t = 0; t < prob->n_terms; t++) {
-    if (prob->terms[t].region >= 0) continue;
-    if (prob->terms[t].form != FEM_WF_ELAST_DOMAIN) return false;
-    n_dom++;
-  }
-  return n_dom > 0;
-}
+// P2-tet elasticity element pass on the tensor cores (tet2_el.cu): *handled = false when the problem has
+// other domain forms or another quadrature order
+int launch_p2_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
+                 double* ek, double* er, cudaStream_t s, bool* handled);
 
 // Morton code of quantised coordinates (about one point per cell)
 struct MortonQ {
@@ -279,28 +265,8 @@ int fem_pattern_stored_prepare(fem_pattern_t p, int with_matrix, void* stream) {
     p->st_ent = keep;
     p->st_n_ent = n_ent;
     p->st_nb = NB;
-    // 3. row order and the flow schedule.  Element items: EI consecutive positions.  A row's "completion" is
-    // the last element item holding one of its elements; rows sorted by completion (Morton order of their
-    // points within) form row items of RI rows; a row item is scheduled LAG element items after its
-    // completion, LAG ≈ 24 MB of stored blocks (the L2 working set between a block's store and its reads).
-    const int EI = 2, RI = 4;  // per warp
-    const int64_t n_ei = (E + EI - 1) / EI;
-    // LAG: at least two superblocks and about the items in flight on a full GPU (~ 24 warps per SM), so a
-    // row item seldom waits (c3: 3552 items, ~39 MB of stored blocks between a store and its reads)
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t LAG = std::max<int64_t>((int64_t)2 * FLOW_SB, (int64_t)sms * 24);
-    std::vector<int32_t> rmin(n_own, INT32_MAX), rmax(n_own, -1);
-    for (int64_t e = 0; e < E; e++) {
-      const int32_t it = epos[e] / EI;
-      for (int a = 0; a < NL; a++) {
-        const int64_t r = m->h_conn[(int64_t)a * E + e];
-        if (r < lo || r >= hi) continue;
-        rmin[r - lo] = std::min(rmin[r - lo], it);
-        rmax[r - lo] = std::max(rmax[r - lo], it);
-      }
-    }
+    // 3. gather order of the rows: Morton order of their points (the warps in flight cover a compact patch,
+    // so the two reads of a symmetric block and the list lines mostly hit L2)
     std::vector<std::pair<uint64_t, int32_t>> rk(n_own);
     {
       const MortonQ Q = morton_q(m, n_own);
@@ -313,54 +279,18 @@ int fem_pattern_stored_prepare(fem_pattern_t p, int with_matrix, void* stream) {
     }
     std::vector<int32_t> rows(n_own);
     for (int64_t i = 0; i < n_own; i++) rows[i] = rk[i].second;
-    std::stable_sort(rows.begin(), rows.end(), [&](int32_t x, int32_t y) { return rmax[x] < rmax[y]; });
-    const int64_t n_ri = (n_own + RI - 1) / RI;
-    std::vector<int32_t> dep(2 * std::max<int64_t>(n_ri, 1));
-    for (int64_t g = 0; g < n_ri; g++) {
-      int32_t a0 = INT32_MAX, a1 = -1;
-      for (int64_t k = g * RI; k < std::min<int64_t>(n_own, (g + 1) * RI); k++) {
-        a0 = std::min(a0, rmin[rows[k]]);
-        a1 = std::max(a1, rmax[rows[k]]);
-      }
-      dep[2 * g] = a1 < 0 ? 0 : a0;
-      dep[2 * g + 1] = a1;  // -1: a row without elements (never: every owned point is in an element)
-    }
-    std::vector<int32_t> sched;
-    sched.reserve(n_ei + n_ri);
-    int64_t g = 0;
-    for (int64_t i = 0; i < n_ei; i++) {
-      sched.push_back((int32_t)i);
-      while (g < n_ri && dep[2 * g + 1] + LAG <= i) sched.push_back((int32_t)(-1 - g++));
-    }
-    while (g < n_ri) sched.push_back((int32_t)(-1 - g++));
-    if (upload(&p->st_rows, rows, s) || upload(&p->st_sched, sched, s) || upload(&p->st_dep, dep, s) ||
-        cudaMalloc(&p->st_done, sizeof(uint32_t) * (n_ei / FLOW_SB + 2)) || cudaMalloc(&p->st_ticket, 4))
-      return fail(FEM_E_OOM, "out of device memory for the schedule");
-    p->st_n_items = (int64_t)sched.size();
-    p->st_n_ei = n_ei;
-    p->st_ei = EI;
-    p->st_ri = RI;
-    // 4. boundary elements (flow path): compact storage of their boundary-term blocks
-    std::vector<int32_t> bmap(E, -1);
-    int64_t n_bnd = 0;
-    for (const auto& be : m->h_bset_elem)
-      for (int32_t e : be)
-        if (bmap[e] < 0) bmap[e] = (int32_t)n_bnd++;
-    p->st_n_bnd = n_bnd;
-    if (upload(&p->st_bmap, bmap, s)) return fail(FEM_E_OOM, "out of device memory for the boundary map");
+    if (upload(&p->st_rows, rows, s)) return fail(FEM_E_OOM, "out of device memory for the row order");
     FEM_CUDA_TRY(cudaStreamSynchronize(s));
   }
   if (!p->st_er) {
-    if (cudaMalloc(&p->st_er, sizeof(double) * (size_t)std::max<int64_t>(E * NL * KH, 1)) ||
-        cudaMalloc(&p->st_fr, sizeof(double) * (size_t)std::max<int64_t>(p->st_n_bnd * NL * KH, 1))) {
+    if (cudaMalloc(&p->st_er, sizeof(double) * (size_t)std::max<int64_t>(E * NL * KH, 1))) {
+      p->st_er = nullptr;
       set_error("fem_pattern_stored_prepare: out of device memory for the element residuals");
       return FEM_E_OOM;
     }
   }
   if (with_matrix && !p->st_ek) {
-    if (cudaMalloc(&p->st_ek, sizeof(double) * (size_t)std::max<int64_t>(E * NB * st_bs(KH), 1)) ||
-        cudaMalloc(&p->st_fk, sizeof(double) * (size_t)std::max<int64_t>(p->st_n_bnd * NB * st_bs(KH), 1))) {
-      cudaFree(p->st_ek);
+    if (cudaMalloc(&p->st_ek, sizeof(double) * (size_t)std::max<int64_t>(E * NB * st_bs(KH), 1))) {
       p->st_ek = nullptr;
       set_error("fem_pattern_stored_prepare: out of device memory for the element blocks (" +
                 std::to_string((double)E * NB * st_bs(KH) * 8 / 1e9) + " GB)");
@@ -412,33 +342,15 @@ int launch_stored(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem
   bool any_bnd = false;
   for (int t = 0; t < prob->n_terms; t++) any_bnd |= prob->terms[t].region >= 0;
   int rc = 0;
-  if (flow_ok(m, prob)) {
-    // boundary terms first, into their compact storage; the flow kernel adds them to the element's blocks
-    const bool bnd = any_bnd && p->st_n_bnd;
-    if (bnd) {
-      if (ek) FEM_CUDA_TRY(cudaMemsetAsync(p->st_fk, 0, sizeof(double) * p->st_n_bnd * p->st_nb * st_bs(KH), s));
-      if (er) FEM_CUDA_TRY(cudaMemsetAsync(p->st_fr, 0, sizeof(double) * p->st_n_bnd * NL * KH, s));
-      rc = stored_facets(m, p, prob, state, ek ? p->st_fk : nullptr, er ? p->st_fr : nullptr, p->st_bmap, s);
-      if (rc) return rc;
-    }
-    FEM_CUDA_TRY(cudaMemsetAsync(p->st_ticket, 0, 4, s));
-    FEM_CUDA_TRY(cudaMemsetAsync(p->st_done, 0, sizeof(uint32_t) * (p->st_n_ei / FLOW_SB + 2), s));
-    FlowParams F;
-    F.sched = p->st_sched; F.n_items = p->st_n_items; F.dep = p->st_dep; F.done = p->st_done;
-    F.ticket = p->st_ticket; F.n_ei = p->st_n_ei; F.ei = p->st_ei; F.ri = p->st_ri;
-    F.E = m->E; F.n_own = m->n_own; F.nnz_s = p->nnz_s;
-    F.eperm = p->st_eperm; F.rows = p->st_rows; F.rowptr_s = p->rowptr_s;
-    F.off = p->st_off; F.ent = p->st_ent; F.roff = p->st_roff; F.rent = p->st_rent;
-    F.bmap = bnd ? p->st_bmap : nullptr;
-    F.fk = (bnd && ek) ? p->st_fk : nullptr;
-    F.fr = (bnd && er) ? p->st_fr : nullptr;
-    F.ek = ek; F.er = er; F.values = values; F.rhs = rhs;
-    return launch_p2_flow(m, prob, F, state, s);
-  }
-  // ---- two-phase path: element pass (domain terms store (the first) or add into the scratch at the
-  // element's position), boundary terms added, then the gather kernel
+  // ---- element pass: domain terms store (the first) or add into the scratch at the element's position
   bool first = true;
-  for (int t = 0; t < prob->n_terms && first; t++) {
+  {
+    bool handled = false;
+    rc = launch_p2_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
+    if (rc) return rc;
+    if (handled) first = false;
+  }
+  for (int t = 0; t < prob->n_terms && first; t++) {  // (skipped when the P2 kernel took them all)
     if (prob->terms[t].region >= 0) continue;
     for (int t2 = t; t2 < prob->n_terms; t2++) {  // every domain term in term order: the first stores
       const fem_term& T2 = prob->terms[t2];

@@ -15,7 +15,6 @@
 #include <string>
 
 #include "tiled.cuh"
-#include "stored.cuh"
 
 namespace fem {
 
@@ -497,23 +496,20 @@ int launch_p2_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_
 }
 
 
-// ---- FEM_SCATTER_STORED, fused element + gather kernel (stored.cu / stored.cuh flow_loop).  Element items:
-// one warp per element, the visit arithmetic above with the element's points gathered straight from HBM
-// (the warp's next element's node ids and coordinates load while the current one computes), the upper
-// blocks a <= b of the symmetric 10 x 10 block matrix K^e (55 of 100: tile 1 where b >= a, tile 2 without
-// its transposes, tile 3 where b >= a) and the residual rows staged in shared memory, the element's
-// boundary-term blocks added, and stored contiguously at its Morton position: ek[pos][blk][i][m],
-// er[pos][a][i].  Row items: the per-slot gathers of stored.cuh.
+// ---- FEM_SCATTER_STORED element pass (stored.cu): one warp per element, the visit arithmetic above with the
+// element's points gathered straight from HBM (the warp's next element's node ids and coordinates load while
+// the current one computes); the upper blocks a <= b of the symmetric 10 x 10 block matrix K^e (55 of 100:
+// tile 1 where b >= a, tile 2 without its transposes, tile 3 where b >= a) and the residual rows are staged
+// in shared memory and stored as one contiguous coalesced stream at the element's Morton position pos:
+// ek[pos][blk][i][m] (blk packed row by row), er[pos][a][i].
 constexpr int P2E_WARPS = 8;
 __device__ __forceinline__ int p2_ublk(int a, int b) { return a * 10 - a * (a - 1) / 2 + (b - a); }
 
 template <bool HAS_V, bool HAS_R>
-__global__ void __launch_bounds__(32 * P2E_WARPS) k_p2_flow(const double* __restrict__ coords, const double* __restrict__ state,
-                                                           const int32_t* __restrict__ conn, int64_t N, P2Coef H,
-                                                           long long* err, const FlowParams F) {
-  const int64_t E = F.E;
-  double* __restrict__ ek = F.ek;
-  double* __restrict__ er = F.er;
+__global__ void __launch_bounds__(32 * P2E_WARPS) k_p2_el(const double* __restrict__ coords, const double* __restrict__ state,
+                                                         const int32_t* __restrict__ conn, int64_t N, int64_t E,
+                                                         const int32_t* __restrict__ eperm, P2Coef H,
+                                                         double* __restrict__ ek, double* __restrict__ er, long long* err) {
   __shared__ double lanetab[32 * P2_LANE_TAB];
   __shared__ double scr[P2E_WARPS][P2_SCRATCH];
   // per-warp staging of the element's 55 blocks (+ 30 residual rows): the lanes' scattered 72-byte blocks
@@ -562,21 +558,19 @@ __global__ void __launch_bounds__(32 * P2E_WARPS) k_p2_flow(const double* __rest
       }
     }
   };
-  const uint64_t keep = st_policy_evict_last();
-  auto elem_item = [&](int item) {
-  const int64_t p0 = (int64_t)item * F.ei, p1 = p0 + F.ei < E ? p0 + F.ei : E;
-  int64_t pos = p0;
+  const int64_t nw = (int64_t)gridDim.x * P2E_WARPS;
+  int64_t pos = (int64_t)blockIdx.x * P2E_WARPS + warp;
   double av[3];
-  load_av(pos < p1 ? (int64_t)__ldg(F.eperm + pos) : -1, av);
-  for (; pos < p1; pos++) {
-    const int64_t e = __ldg(F.eperm + pos);
-    const int64_t pn = pos + 1;
+  load_av(pos < E ? (int64_t)__ldg(eperm + pos) : -1, av);
+  for (; pos < E; pos += nw) {
+    const int64_t e = __ldg(eperm + pos);
+    const int64_t pn = pos + nw;
     double C2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int s = 0; s < 3; s++)
 #pragma unroll
       for (int t = 0; t < 2; t++) dmma884_t2(C2[t], av[s], L[32 * (s * 2 + t)]);
-    load_av(pn < p1 ? (int64_t)__ldg(F.eperm + pn) : -1, av);  // prefetch: in flight while this element computes
+    load_av(pn < E ? (int64_t)__ldg(eperm + pn) : -1, av);  // prefetch: in flight while this element computes
     if (r < 6) {
 #pragma unroll
       for (int t = 0; t < 2; t++)
@@ -728,57 +722,49 @@ __global__ void __launch_bounds__(32 * P2E_WARPS) k_p2_flow(const double* __rest
       }
     }
     __syncwarp();
-    const int bi = F.bmap ? __ldg(F.bmap + e) : -1;  // the element's boundary-term blocks, if any
-    if constexpr (HAS_V) {  // 55 blocks of 12 doubles (9 + pad): 256-bit stores, 3 per block
-      double* dst = ek + pos * (55 * 12);
-      const double* fb = bi >= 0 ? F.fk + (int64_t)bi * (55 * 12) : nullptr;
-      for (int g = lane; g < 55 * 3; g += 32) {
-        const int blk = g / 3, q = g - 3 * blk;
-        const double* sv = stage[warp] + blk * 9 + 4 * q;
-        double v[4];
-#pragma unroll
-        for (int i = 0; i < 4; i++) v[i] = (q < 2 || i == 0) ? sv[i] : 0.0;
-        if (fb) {
-#pragma unroll
-          for (int i = 0; i < 4; i++) v[i] += __ldg(fb + 12 * blk + 4 * q + i);
-        }
-        st_st4(dst + 12 * blk + 4 * q, v[0], v[1], v[2], v[3]);
-      }
+    if constexpr (HAS_V) {
+      double* dst = ek + pos * (55 * 9);
+      for (int k = lane; k < 55 * 9; k += 32) dst[k] = stage[warp][k];
     }
     if constexpr (HAS_R) {
-      const double* fb = bi >= 0 ? F.fr + (int64_t)bi * 30 : nullptr;
-      if (lane < 30) st_store_keep(er + pos * 30 + lane, fb ? stage[warp][55 * 9 + lane] + __ldg(fb + lane) : stage[warp][55 * 9 + lane], keep);
+      if (lane < 30) er[pos * 30 + lane] = stage[warp][55 * 9 + lane];
     }
     __syncwarp();  // the scratch and the stage are rewritten by the next element
   }
-  };
-  flow_loop<3>(F, elem_item);
 }
 
-// P2 tets, 4-point rule, every domain term ELAST_DOMAIN (stored.cu checks): the fused stored-mode kernel.
-int launch_p2_flow(const fem_mesh_s* m, const fem_problem* prob, const FlowParams& F, const double* state,
-                   cudaStream_t s) {
+// P2 tets, 4-point rule, every domain term ELAST_DOMAIN: the stored-mode element pass (all domain terms).
+int launch_p2_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
+                 double* ek, double* er, cudaStream_t s, bool* handled) {
+  *handled = false;
+  if (m->etype != ET_TET || m->order != 2 || m->kh != 3 || m->physics != FEM_ELASTICITY || prob->quad_order != 2)
+    return 0;
   P2Coef H = {0, 0, 0, 0};
+  int n_dom = 0;
   for (int t = 0; t < prob->n_terms; t++) {
     const fem_term& T = prob->terms[t];
     if (T.region >= 0) continue;
+    if (T.form != FEM_WF_ELAST_DOMAIN) return 0;
     const FormArgs Fa = make_form_args(prob, T);
     H.cl += Fa.f0 * Fa.lam; H.cm += Fa.f0 * Fa.mu; H.sl += Fa.lam; H.sm += Fa.mu;
+    n_dom++;
   }
-  if (F.n_items == 0 || F.n_ei == 0) return 0;
+  if (!n_dom) return 0;
+  *handled = true;
+  if (m->E == 0) return 0;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   auto go = [&](auto kern) -> int {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * P2E_WARPS, 0);
-    const int64_t grid = std::min<int64_t>((F.n_items + P2E_WARPS - 1) / P2E_WARPS, (int64_t)sms * std::max(per_sm, 1));
-    kern<<<(unsigned)grid, 32 * P2E_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, H, m->err, F);
+    const int64_t grid = std::min<int64_t>((m->E + P2E_WARPS - 1) / P2E_WARPS, (int64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, 32 * P2E_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, m->E, eperm, H, ek, er, m->err);
     FEM_CUDA_TRY(cudaGetLastError());
     return 0;
   };
-  if (F.ek && F.er) return go(k_p2_flow<true, true>);
-  if (F.ek) return go(k_p2_flow<true, false>);
-  return go(k_p2_flow<false, true>);
+  if (ek && er) return go(k_p2_el<true, true>);
+  if (ek) return go(k_p2_el<true, false>);
+  return go(k_p2_el<false, true>);
 }
 
 }  // namespace fem
