@@ -17,21 +17,29 @@ for row in det[1:]:
         print(f"{d['Metric Name']:40s} {d['Metric Value']:>14s} {d['Metric Unit']}")
 print('kernel:', kname[:120] if kname else None)
 raw = list(csv.reader(io.StringIO(run('--page', 'raw', '--csv'))))
-d = dict(zip(raw[0], raw[2]))
-for k in ['dram__bytes_read.sum', 'dram__bytes_write.sum', 'gpu__time_duration.sum',
-          'smsp__sass_thread_inst_executed_op_dfma_pred_on.sum', 'smsp__sass_thread_inst_executed_op_dadd_pred_on.sum',
-          'smsp__sass_thread_inst_executed_op_dmul_pred_on.sum', 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
-          'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active', 'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum',
-          'smsp__inst_executed.sum', 'sm__warps_active.avg.pct_of_peak_sustained_active']:
-    if k in d: print(f'{k:60s} {d[k]} {raw[1][raw[0].index(k)]}')
-st = {k: v for k, v in d.items() if k.startswith('smsp__pcsamp_warps_issue_stalled') and not k.endswith('not_issued')}
-tot = sum(float(v.replace(',', '') or 0) for v in st.values())
-print('stall samples (share):')
-for k, v in sorted(st.items(), key=lambda kv: -float(kv[1].replace(',', '') or 0))[:10]:
-    print(f'   {k.replace("smsp__pcsamp_warps_issue_stalled_", ""):28s} {float(v.replace(",", ""))/max(tot,1):6.1%}')
+for row in raw[2:]:  # one row per captured launch
+    d = dict(zip(raw[0], row))
+    print('== raw metrics of', d.get('Kernel Name', '?')[:100])
+    for k in ['dram__bytes_read.sum', 'dram__bytes_write.sum', 'gpu__time_duration.sum',
+              'smsp__sass_thread_inst_executed_op_dfma_pred_on.sum', 'smsp__sass_thread_inst_executed_op_dadd_pred_on.sum',
+              'smsp__sass_thread_inst_executed_op_dmul_pred_on.sum', 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
+              'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active', 'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum',
+              'smsp__inst_executed.sum', 'sm__warps_active.avg.pct_of_peak_sustained_active']:
+        if k in d: print(f'{k:60s} {d[k]} {raw[1][raw[0].index(k)]}')
+    st = {k: v for k, v in d.items() if k.startswith('smsp__pcsamp_warps_issue_stalled') and not k.endswith('not_issued')}
+    tot = sum(float(v.replace(',', '') or 0) for v in st.values())
+    print('stall samples (share):')
+    for k, v in sorted(st.items(), key=lambda kv: -float(kv[1].replace(',', '') or 0))[:10]:
+        print(f'   {k.replace("smsp__pcsamp_warps_issue_stalled_", ""):28s} {float(v.replace(",", ""))/max(tot,1):6.1%}')
 src = list(csv.reader(io.StringIO(run('--page', 'source', '--csv', '--print-source', 'sass'))))
 h = src[1]; ix = {x: i for i, x in enumerate(h)}; rows = src[2:]
-tot = sum(int(r[ix['Warp Stall Sampling (All Samples)']] or 0) for r in rows)
+def _int(x):
+    try:
+        return int(x or 0)
+    except ValueError:
+        return 0
+rows = [r for r in rows if len(r) > ix['Warp Stall Sampling (All Samples)'] and _int(r[ix['Warp Stall Sampling (All Samples)']]) >= 0 and r[ix['Address']].startswith('0x')]
+tot = sum(_int(r[ix['Warp Stall Sampling (All Samples)']]) for r in rows)
 print(f'top SASS stall sites ({tot} samples):')
-for r in sorted(rows, key=lambda r: -int(r[ix['Warp Stall Sampling (All Samples)']] or 0))[:ntop]:
-    print(f"  {r[ix['Address']][-5:]} {int(r[ix['Warp Stall Sampling (All Samples)']])/tot:6.1%} exec={r[ix['Instructions Executed']]:>9s} {r[ix['Source']][:80]}")
+for r in sorted(rows, key=lambda r: -_int(r[ix['Warp Stall Sampling (All Samples)']]))[:ntop]:
+    print(f"  {r[ix['Address']][-5:]} {_int(r[ix['Warp Stall Sampling (All Samples)']])/max(tot,1):6.1%} exec={r[ix['Instructions Executed']]:>9s} {r[ix['Source']][:80]}")
