@@ -125,6 +125,7 @@ def extra_entry(name, variant, scatter, steps, warmup):
                    "hbm_frac": ab / (ms * 1e-3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)),
                    "kernel": (TILED_KERNEL.get(name) if sc == "tiled" else
                               "k_p2_el + k_st_gather (element-stored, per-slot gather)" if sc == "stored" and name == "c3" else
+                              "k_ns_el + k_st_gather (element-stored, per-slot gather)" if sc == "stored" and name == "c4" else
                               f"{sc} path"),
                    "deterministic": sc in ("tiled", "coloured", "stored")}
     status = S.status()
@@ -413,7 +414,7 @@ def main():
         torch.cuda.empty_cache()
         extras = {}
         for nm, var, scs in [("c2", "structured", ["tiled"]), ("c3", "structured", ["tiled", "tiled_unordered", "stored"]),
-                             ("c4", "structured", ["tiled", "tiled_unordered"]), ("c5", "perturbed", ["tiled"])]:
+                             ("c4", "structured", ["tiled", "tiled_unordered", "stored"]), ("c5", "perturbed", ["tiled"])]:
             try:
                 extras[f"{nm}/{var}"] = extra_entry(nm, var, scs, max(3, min(args.steps, 10)), 3)
             except Exception as exc:  # reported, never hidden

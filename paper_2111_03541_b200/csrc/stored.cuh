@@ -8,6 +8,13 @@ namespace fem {
 // Stored block stride (doubles): the κ̂² values of a block, contiguous.
 __host__ __device__ constexpr int st_bs(int KH) { return KH * KH; }
 
+__device__ __forceinline__ void st_st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void st_ld4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
 // One owned row li: lane per CSR slot of the row, the slot's stored blocks summed in list order (GU per
 // trip, all loads first), κ̂² values written.
 template <int KH>
@@ -22,7 +29,7 @@ __device__ __forceinline__ void st_gather_row(int64_t li, const int64_t* __restr
 #pragma unroll
     for (int k = 0; k < KH * KH; k++) acc[k] = 0.0;
     const uint32_t j0 = __ldg(off + s), j1 = __ldg(off + s + 1);
-    constexpr int GU = KH >= 3 ? 2 : 4;
+    constexpr int GU = KH >= 3 ? 2 : 4;  // (κ̂ = 4: 32 doubles in flight)
     for (uint32_t j = j0; j < j1; j += GU) {
       uint32_t x[GU];
 #pragma unroll
@@ -32,8 +39,13 @@ __device__ __forceinline__ void st_gather_row(int64_t li, const int64_t* __restr
       for (int u = 0; u < GU; u++) {
         // past the list end: block 0 (a valid address; the values are not added)
         const double* src = ek + (int64_t)(j + u < j1 ? (x[u] >> 1) : 0u) * st_bs(KH);
+        if constexpr (KH * KH % 4 == 0) {  // κ̂ = 2, 4: blocks are whole 32-byte sectors, 256-bit loads
 #pragma unroll
-        for (int k = 0; k < KH * KH; k++) v[u][k] = __ldg(src + k);
+          for (int q = 0; q < KH * KH / 4; q++) st_ld4(src + 4 * q, v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < KH * KH; k++) v[u][k] = __ldg(src + k);
+        }
       }
 #pragma unroll
       for (int u = 0; u < GU; u++) {

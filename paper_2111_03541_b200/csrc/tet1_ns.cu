@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "stored.cuh"
 #include "tiled.cuh"
 
 namespace fem {
@@ -37,27 +38,26 @@ constexpr int NSM_R0 = 99;   // R0[i] = Σ_γ w Rm_i(γ)                     (3)
 constexpr int NSM_P0 = 102;  // P0 = Σ_γ w p(γ)                           (1)
 constexpr int NS_SC = 104;   // doubles per visit (even)
 
-template <bool DET>
-__device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& D, const NsCoef& c, int v0, int nv,
-                                          double* scw, const uint8_t* vseq, int* turn) {
+// The per-element arithmetic of a P1 NS visit, for the two elements of a warp (half-warp h = lane >> 4 takes
+// one; called by all 32 lanes).  val(k, n): component k (x, y, z, u1, u2, u3, p) of node n of the half's
+// element; sc: the half's NS_SC scratch doubles.  Returns false when some lane's element has det J <= 0
+// (*bad set on that lane; acc/res untouched), else lane (a, b) = (l16 >> 2, l16 & 3) receives the 4x4
+// block of the pair (a, b) summed over the points (without f0) and the residual entry of row (a, κ0 = b).
+template <class Val>
+__device__ __forceinline__ bool ns_compute(const NsCoef& c, double* sc, bool valid, Val&& val, bool* bad_out,
+                                           double (&acc)[4][4], double& res) {
   const int lane = threadIdx.x & 31;
-  const int h = lane >> 4, l16 = lane & 15;
-  const int v = v0 + h;
-  const bool valid = v < nv;
-  const int vv = valid ? v : v0;
+  const int l16 = lane & 15;
   const double al = 0.13819660112501051518, be = 0.58541019662496845446;  // (5-√5)/20, (5+3√5)/20
-  double* sc = scw + h * NS_SC;
   // ---- phase 1: the 16 lanes of each half-warp compute the visit's constants (affine P1 tet): the
   // geometry redundantly (SIMT: same issue cost as one lane), the per-lane values split over the lanes
   bool bad = false;
   {
     double X[4][3];
 #pragma unroll
-    for (int n = 0; n < 4; n++) {
-      const int hh = (uint16_t)D.vhal[vv * 4 + n];
+    for (int n = 0; n < 4; n++)
 #pragma unroll
-      for (int d = 0; d < 3; d++) X[n][d] = D.hdat[d * D.H + hh];
-    }
+      for (int d = 0; d < 3; d++) X[n][d] = val(d, n);
     double J[3][3];
 #pragma unroll
     for (int i = 0; i < 3; i++)
@@ -91,10 +91,7 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
       const int k = l16 / 3, i = l16 % 3;
       double g = 0.0;
 #pragma unroll
-      for (int n = 0; n < 4; n++) {
-        const int hh = (uint16_t)D.vhal[vv * 4 + n];
-        g = fma(D.hdat[(3 + k) * D.H + hh], G[n][i], g);
-      }
+      for (int n = 0; n < 4; n++) g = fma(val(3 + k, n), G[n][i], g);
       sc[12 + l16] = g;
       double gsel = G[0][0];
 #pragma unroll
@@ -109,8 +106,7 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
       double us = 0.0, uq = 0.0;
 #pragma unroll
       for (int n = 0; n < 4; n++) {
-        const int hh = (uint16_t)D.vhal[vv * 4 + n];
-        const double U = D.hdat[(3 + k) * D.H + hh];
+        const double U = val(3 + k, n);
         us += U;
         if (n == q) uq = U;
       }
@@ -168,27 +164,11 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
       }
     }
   }
-  if (__any_sync(0xffffffffu, bad)) {
-    if (bad) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)D.vid[v]);
-    if constexpr (DET) {  // still pass the turns on, or later visits of these rows would wait forever
-      const int a = l16 >> 2, li = D.vown[vv * 4 + a];
-      if (valid && li >= 0 && (l16 & 3) == 0) {
-        volatile int* tp = turn + li;
-        const int t = vseq[vv * 4 + a];
-        while (*tp != t) {
-        }
-        __threadfence_block();
-        *tp = t + 1;
-      }
-    }
-    __syncwarp();
-    return;
-  }
+  *bad_out = bad;
+  if (__any_sync(0xffffffffu, bad)) return false;
   __syncwarp();
-  // ---- phase 2: lane (a, b): the 4x4 block of the pair and the residual row (a, κ0 = b)
   const double rho = c.rho, mu = c.mu, tm = c.tm, tc = c.tc;
   const int a = l16 >> 2, b = l16 & 3;
-  const int li = D.vown[vv * 4 + a];
   double Ga[3], Gb[3];
 #pragma unroll
   for (int i = 0; i < 3; i++) { Ga[i] = sc[a * 3 + i]; Gb[i] = sc[b * 3 + i]; }
@@ -216,7 +196,6 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
     for (int j = 0; j < 3; j++) t = fma(UU[k * 3 + j], Gb[j], t);
     s2 = fma(Ga[k], t, s2);
   }
-  double acc[4][4];
   const double diag = -rho * s1 + mu * W * GaGb + tm * rho * rho * s2;
 #pragma unroll
   for (int i = 0; i < 3; i++) {
@@ -231,7 +210,6 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
     acc[3][i] = Wq * Gb[i] + tm * rho * (Wq * smv[i] + Ga[i] * bU0);
   }
   acc[3][3] = tm * W * GaGb;
-  double res;
   if (b < 3) {  // residual row (a, u_b): BASE + SUPG of NS_domain
     const int i = b;
     res = -Ga[i] * sc[NSM_P0] + tc * W * Ga[i] * Rc;
@@ -241,6 +219,40 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
   } else {      // residual row (a, p)
     res = Wq * Rc + tm * (Ga[0] * sc[NSM_R0] + Ga[1] * sc[NSM_R0 + 1] + Ga[2] * sc[NSM_R0 + 2]);
   }
+  return true;
+}
+
+template <bool DET>
+__device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& D, const NsCoef& c, int v0, int nv,
+                                          double* scw, const uint8_t* vseq, int* turn) {
+  const int lane = threadIdx.x & 31;
+  const int h = lane >> 4, l16 = lane & 15;
+  const int v = v0 + h;
+  const bool valid = v < nv;
+  const int vv = valid ? v : v0;
+  double* sc = scw + h * NS_SC;
+  double acc[4][4], res = 0.0;
+  bool bad = false;
+  const bool ok = ns_compute(c, sc, valid, [&](int k, int n) { return D.hdat[k * D.H + (uint16_t)D.vhal[vv * 4 + n]]; },
+                             &bad, acc, res);
+  if (!ok) {
+    if (bad) atomicCAS((unsigned long long*)P.err, (unsigned long long)(-1LL), (unsigned long long)D.vid[v]);
+    if constexpr (DET) {  // still pass the turns on, or later visits of these rows would wait forever
+      const int a = l16 >> 2, li = D.vown[vv * 4 + a];
+      if (valid && li >= 0 && (l16 & 3) == 0) {
+        volatile int* tp = turn + li;
+        const int t = vseq[vv * 4 + a];
+        while (*tp != t) {
+        }
+        __threadfence_block();
+        *tp = t + 1;
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  const int a = l16 >> 2, b = l16 & 3;
+  const int li = D.vown[vv * 4 + a];
   if constexpr (DET) {
     // ordered: visit v takes its turn (vseq) on the accumulator row of each owned node, so every entry
     // sums its contributions in record order with plain read-modify-writes (bit-identical run to run).
@@ -425,6 +437,93 @@ int launch_ns_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_
   else k_ns_rec<false><<<(unsigned)grid, TILED_THREADS, smem, s>>>(P);
   FEM_CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+
+// ---- FEM_SCATTER_STORED element pass (stored.cu): the visit arithmetic of ns_compute for one element per
+// half-warp, its points gathered straight from HBM into the half's scratch; lane (a, b) stores the 4x4 block
+// (a, b) — f0·K, 16 doubles, four 256-bit stores — at ek[pos][a·4 + b] (all 16 blocks: NS is not symmetric)
+// and the residual entry (a, κ0 = b) at er[pos][a][b]; the element's 16 lanes write 2 KB contiguously.
+constexpr int NSE_WARPS = 8;
+template <bool HAS_V, bool HAS_R>
+__global__ void __launch_bounds__(32 * NSE_WARPS) k_ns_el(const double* __restrict__ coords, const double* __restrict__ state,
+                                                         const int32_t* __restrict__ conn, int64_t N, int64_t E,
+                                                         const int32_t* __restrict__ eperm, NsCoef cf,
+                                                         double* __restrict__ ek, double* __restrict__ er, long long* err) {
+  __shared__ double scr[NSE_WARPS][2][NS_SC];
+  __shared__ double nd[NSE_WARPS][2][7 * 4];  // component-major point data of the half's element
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, h = lane >> 4, l16 = lane & 15;
+  const int64_t n_half = (int64_t)gridDim.x * NSE_WARPS * 2;
+  const int64_t first = ((int64_t)blockIdx.x * NSE_WARPS + warp) * 2 + h;
+  double* sc = scr[warp][h];
+  double* x = nd[warp][h];
+  // the warp loops while either half has an element (ns_compute is warp-collective)
+  for (int64_t base = first - h; base < E; base += n_half) {
+    const int64_t pos = base + h;
+    const bool valid = pos < E;
+    const int64_t e = valid ? __ldg(eperm + pos) : 0;
+    int node = 0;
+    if (l16 < 4) node = valid ? __ldg(conn + (int64_t)l16 * E + e) : 0;
+#pragma unroll
+    for (int k = 0; k < 2; k++) {  // 28 values over the 16 lanes: (component, node) = divmod(idx, 4)
+      const int idx = l16 + 16 * k;
+      const int src = (lane & 16) | (idx & 3);
+      const int nn = __shfl_sync(0xffffffffu, node, src);
+      if (idx < 28) {
+        const int comp = idx >> 2;
+        x[idx] = !valid ? (comp < 3 ? (double)((idx & 3) == comp + 1) : 0.0)  // (unit tet: det > 0)
+                        : comp < 3 ? __ldg(coords + (int64_t)comp * N + nn) : __ldg(state + (int64_t)(comp - 3) * N + nn);
+      }
+    }
+    __syncwarp();
+    double acc[4][4], res = 0.0;
+    bool bad = false;
+    const bool ok = ns_compute(cf, sc, valid, [&](int k, int n) { return x[k * 4 + n]; }, &bad, acc, res);
+    if (!ok) {
+      if (bad) atomicCAS((unsigned long long*)err, (unsigned long long)(-1LL), (unsigned long long)e);
+      __syncwarp();
+      continue;
+    }
+    if (valid) {
+      if constexpr (HAS_V) {
+        double* dst = ek + (pos * 16 + l16) * 16;
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          st_st4(dst + 4 * i, cf.f0 * acc[i][0], cf.f0 * acc[i][1], cf.f0 * acc[i][2], cf.f0 * acc[i][3]);
+      }
+      if constexpr (HAS_R) er[pos * 16 + l16] = res;
+    }
+    __syncwarp();  // the scratch is rewritten by the next element
+  }
+}
+
+// NS on P1 tets, 4-point rule, exactly one domain term NS_DOMAIN: the stored-mode element pass.
+int launch_ns_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
+                 double* ek, double* er, cudaStream_t s, bool* handled) {
+  *handled = false;
+  if (m->etype != ET_TET || m->order != 1 || m->kh != 4 || m->physics != FEM_NS || prob->quad_order != 2) return 0;
+  int n_dom = 0, t_dom = -1;
+  for (int t = 0; t < prob->n_terms; t++)
+    if (prob->terms[t].region < 0) { n_dom++; t_dom = t; }
+  if (n_dom != 1 || prob->terms[t_dom].form != FEM_WF_NS_DOMAIN) return 0;
+  *handled = true;
+  if (m->E == 0) return 0;
+  const FormArgs F = make_form_args(prob, prob->terms[t_dom]);
+  NsCoef cf;
+  cf.rho = F.p[0]; cf.mu = F.p[1]; cf.tm = F.p[2]; cf.tc = F.p[3]; cf.f0 = F.f0;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto go = [&](auto kern) -> int {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NSE_WARPS, 0);
+    const int64_t grid = std::min<int64_t>((m->E + 2 * NSE_WARPS - 1) / (2 * NSE_WARPS), (int64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, 32 * NSE_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, m->E, eperm, cf, ek, er, m->err);
+    FEM_CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  if (ek && er) return go(k_ns_el<true, true>);
+  if (ek) return go(k_ns_el<true, false>);
+  return go(k_ns_el<false, true>);
 }
 
 }  // namespace fem
