@@ -262,8 +262,7 @@ __device__ __forceinline__ void ns_visit2(const TiledParams& P, const TileSmem& 
     int my_turn = 0;
     if (valid && li >= 0) {
       my_turn = vseq[vv * 4 + a];
-      while (*reinterpret_cast<volatile int*>(turn + li) != my_turn) {
-      }
+      while (*reinterpret_cast<volatile int*>(turn + li) != my_turn) __nanosleep(32);  // (frees issue slots)
       __threadfence_block();
       if (P.values) {
         const int d = D.tdeg[li], sr = acc_row_stride(4, d, P.nnz_s);
