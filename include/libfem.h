@@ -78,7 +78,9 @@ extern "C" {
  *                        node tiles.  Residual-only calls on tetrahedra use the coloured element pass (cheaper
  *                        than the tiles for rows alone; still deterministic).  FEM_E_UNSUPPORTED (never a silent
  *                        fallback) for elements without a tile kernel (quadratic cubes) or a tile point touched
- *                        by more than 255 visits.
+ *                        by more than 255 visits.  Calls on one pattern use its schedule's scratch (ring
+ *                        records; on renumbered lattice meshes a lattice-ordered state copy): issue them on
+ *                        one stream (or otherwise in order).
  * FEM_SCATTER_TILED_UNORDERED  owner gather with shared-memory fp64 atomics where a kernel has them (P2 and
  *                        NS tets, generic tiles; hex as TILED): faster, summation order varies run to run.
  *                        Residual-only calls on tetrahedra use the atomic element pass.
@@ -87,7 +89,8 @@ extern "C" {
  *                        blocks of the elements that contain its two points in ELEMENT ORDER and every row its
  *                        elements' residual rows: no atomics, bit-identical run to run, complete rows written
  *                        (accumulate must be 0).  Needs fem_pattern_stored_prepare first (FEM_E_INVALID_ARG
- *                        otherwise).  Every element type and physics. */
+ *                        otherwise).  Every element type and physics.  The element scratch belongs to the
+ *                        pattern: issue the calls on one pattern on one stream. */
 #define FEM_SCATTER_ATOMIC 0
 #define FEM_SCATTER_COLOURED 1
 #define FEM_SCATTER_TILED 2

@@ -69,6 +69,13 @@ struct TileSchedule {
   int sweep_sr = 0;                // ring sub-row stride (81 or 82: fixed 27-column layout, parity of 3·nnz_s)
   int64_t n_seq = 0;
   int64_t* seq_off = nullptr;     // device [n_seq+1]: records of sequence q are [seq_off[q], seq_off[q+1])
+  // renumbered meshes (points not in lattice order): the sweep stages its halo from copies of the point data
+  // in lattice order, so the gathers of a step are contiguous; sw_lperm[k] = the point at lattice rank k,
+  // sw_pcoords = coordinates in that order (built once), sw_pstate = the state, permuted per call
+  int32_t* sw_lperm = nullptr;
+  double* sw_pcoords = nullptr;
+  double* sw_pstate = nullptr;
+  int sw_pstate_comps = 0;
 };
 
 // Packed per-tile record: header int32 {T, H, nv, nruns, acc_n, fac_mask, 0, 0} followed by
@@ -222,6 +229,8 @@ void stored_free(fem_pattern_s* p);
 int launch_q2_elast(const AsmArgs& A, int* handled);
 // z-sweep schedule for Q1-hex elasticity on lattice meshes (sweep.cu); FEM_E_UNSUPPORTED: not applicable
 int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s);
+// dst[c][k] = src[c][perm[k]] (sweep.cu)
+int perm_gather(const double* src, double* dst, const int32_t* perm, int64_t n, int ncomp, cudaStream_t s);
 int launch_tiled(const fem_mesh_s* m, const fem_pattern_s* pat, const fem_problem* prob,
                  const double* state, double* values, double* rhs, bool det, cudaStream_t stream);
 int pattern_build(fem_mesh_s* m, cudaStream_t stream, fem_pattern_s* p);

@@ -1131,6 +1131,17 @@ static int run_hex_sweep(TiledParams& P, const TileSchedule& T, cudaStream_t s) 
   }
   P.seq_off = T.seq_off;
   P.n_seq = T.n_seq;
+  if (T.sw_lperm) {  // renumbered mesh: the halo ids are lattice ranks; stage from lattice-ordered copies
+    const int ncomp = 3 * (P.nu_hat >= 1 ? 2 : 1);
+    if (ncomp > T.sw_pstate_comps) {
+      set_error("hex sweep kernel: state components exceed the lattice-ordered copy");
+      return FEM_E_UNSUPPORTED;
+    }
+    const int rc = perm_gather(P.state, T.sw_pstate, T.sw_lperm, P.N, ncomp, s);
+    if (rc) return rc;
+    P.coords = T.sw_pcoords;
+    P.state = T.sw_pstate;
+  }
   P.rec = T.rec;
   P.rec_off = T.rec_off;
   P.n_tiles = T.n_tiles;

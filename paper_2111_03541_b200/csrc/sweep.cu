@@ -110,6 +110,19 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
     if (slot >= 0) return FEM_E_UNSUPPORTED;
     slot = (int32_t)e;
   }
+  // lattice rank of every point: renumbered meshes stage their halo from lattice-ordered copies
+  std::vector<int32_t> lpos(N), lperm;
+  bool lat_ident = true;
+  {
+    int32_t k = 0;
+    for (size_t q = 0; q < node_at.size(); q++)
+      if (node_at[q] >= 0) lpos[node_at[q]] = k++;
+    for (int64_t i = 0; i < N && lat_ident; i++) lat_ident = lpos[i] == i;
+    if (!lat_ident) {
+      lperm.resize(N);
+      for (int64_t i = 0; i < N; i++) lperm[lpos[i]] = (int32_t)i;
+    }
+  }
   // ---- 2. pattern rows (degrees, row starts) and boundary facets per element
   std::vector<int64_t> rps(n_own + 1);
   FEM_CUDA_TRY(cudaMemcpyAsync(rps.data(), p->rowptr_s, sizeof(int64_t) * (n_own + 1), cudaMemcpyDeviceToHost, s));
@@ -298,7 +311,12 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
               }
           }
           o_toff[TR] = (int32_t)(2 * SLOT);
-          memcpy(r + L.o_hnode, halo.data(), sizeof(int32_t) * H);
+          if (lat_ident) {
+            memcpy(r + L.o_hnode, halo.data(), sizeof(int32_t) * H);
+          } else {
+            int32_t* hn = reinterpret_cast<int32_t*>(r + L.o_hnode);
+            for (int i = 0; i < H; i++) hn[i] = lpos[halo[i]];
+          }
           memcpy(r + L.o_run, run.data(), sizeof(int32_t) * run.size());
           int32_t* o_velem = reinterpret_cast<int32_t*>(r + L.o_velem);
           uint16_t* o_vhal = reinterpret_cast<uint16_t*>(r + L.o_vhal);
@@ -436,10 +454,37 @@ int sweep_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
                                                  m->conn, p->rowptr_s, E, lo, hi);
     FEM_CUDA_TRY(cudaGetLastError());
   }
+  if (!lat_ident) {  // lattice-ordered copies: coordinates once, the state buffer for the per-call gather
+    T.sw_pstate_comps = 2 * KH;  // d (and ḋ with ν̂ >= 1)
+    FEM_CUDA_TRY(cudaMalloc(&T.sw_lperm, sizeof(int32_t) * N));
+    FEM_CUDA_TRY(cudaMalloc(&T.sw_pcoords, sizeof(double) * 3 * N));
+    FEM_CUDA_TRY(cudaMalloc(&T.sw_pstate, sizeof(double) * T.sw_pstate_comps * N));
+    FEM_CUDA_TRY(cudaMemcpy(T.sw_lperm, lperm.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    const int rc = perm_gather(m->coords, T.sw_pcoords, T.sw_lperm, N, 3, s);
+    if (rc) return rc;
+  }
   FEM_CUDA_TRY(cudaStreamSynchronize(s));
   cudaFree(d_vis);
   cudaFree(d_vloc);
   cudaFree(d_vfst);
+  return 0;
+}
+
+// dst[c][k] = src[c][perm[k]] for c < ncomp (component-major arrays of n points)
+__global__ void k_perm_gather(const double* __restrict__ src, double* __restrict__ dst, const int32_t* __restrict__ perm,
+                              int64_t n, int ncomp) {
+  const int64_t tot = n * ncomp;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / n, k = t - c * n;
+    dst[t] = __ldg(src + c * n + __ldg(perm + k));
+  }
+}
+int perm_gather(const double* src, double* dst, const int32_t* perm, int64_t n, int ncomp, cudaStream_t s) {
+  const int64_t tot = n * ncomp;
+  if (tot <= 0) return 0;
+  const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 64);
+  k_perm_gather<<<(unsigned)blocks, 256, 0, s>>>(src, dst, perm, n, ncomp);
+  FEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }
 

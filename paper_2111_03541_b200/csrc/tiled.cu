@@ -82,6 +82,9 @@ static void free_visits(VisitList& V) {
 
 void tiles_free(TileSchedule& T) {
   cudaFree(T.seq_off);
+  cudaFree(T.sw_lperm);
+  cudaFree(T.sw_pcoords);
+  cudaFree(T.sw_pstate);
   cudaFree(T.rec);
   cudaFree(T.rec_off);
   cudaFree(T.halo_off);

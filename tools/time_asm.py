@@ -1,4 +1,4 @@
-"""Dev timing helper: python tools/time_asm.py c5 [atomic|coloured|tiled] [dims...]"""
+"""Dev timing helper: python tools/time_asm.py c5[p] [atomic,coloured,tiled,...] [dims...]  (c5p: perturbed variant)"""
 import sys, time
 import numpy as np
 import torch
@@ -9,7 +9,9 @@ from paper_2111_03541_b200 import FemSystem
 name = sys.argv[1]
 modes = sys.argv[2].split(',') if len(sys.argv) > 2 else ['atomic']
 dims = tuple(int(x) for x in sys.argv[3:]) or None
-t0 = time.time(); m, p = make_config(name, 'structured', dims); st = make_state(name, m, p)
+variant = 'perturbed' if name.endswith('p') and name[:-1] in ('c2', 'c3', 'c4', 'c5') else 'structured'
+name = name[:-1] if variant == 'perturbed' else name
+t0 = time.time(); m, p = make_config(name, variant, dims); st = make_state(name, m, p)
 print(f'{name} E={m.n_elems} N={m.n_nodes} gen {time.time()-t0:.1f}s', flush=True)
 t0 = time.time(); S = FemSystem(m, p); torch.cuda.synchronize()
 print(f'mesh+pattern {time.time()-t0:.1f}s nnz={S.nnz} colours={S.info()}', flush=True)
