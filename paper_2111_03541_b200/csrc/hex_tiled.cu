@@ -325,7 +325,7 @@ __device__ __forceinline__ GeoFrag geo_frag() {
 // arrives by one TMA bulk copy and its halo points by LDGSTS while the current tile computes.
 __device__ __forceinline__ void gather_halo(const TiledParams& P, const uint8_t* rec, double* hbuf) {
   const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
-  const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
+  const int H = hdr[1];
   const RecLayout L = rec_layout_hdr(8, hdr);
   const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
   for (int c = 0; c < P.hcomp; c++) {  // component-major: no integer division per element
@@ -1271,6 +1271,207 @@ int launch_hex_tiled(TiledParams& P, const TileSchedule& T, int kh, bool det, cu
   }
   if (det) return kh == 3 ? run_hex_rec<3, true>(P, T, s) : run_hex_rec<1, true>(P, T, s);
   return kh == 3 ? run_hex_rec<3, false>(P, T, s) : run_hex_rec<1, false>(P, T, s);
+}
+
+
+// ---- FEM_SCATTER_STORED element pass for Q1-hex elasticity (stored.cu): one warp per element, the visit
+// arithmetic of hex_visit_el2 (geometry GEMM, per-point records with J^-1, w and w σ, the residual GEMM,
+// the 18-DMMA Gram and K) with the element's points gathered straight from HBM; the upper blocks a <= b
+// (36 of 64) and the 24 residual rows are staged in shared memory and stored as one coalesced stream at the
+// element's Morton position: ek[pos][blk][i][m], er[pos][a][i].
+constexpr int HXE_WARPS = 8;
+template <bool HAS_V, bool HAS_R>
+__global__ void __launch_bounds__(32 * HXE_WARPS) k_hex_el(const double* __restrict__ coords, const double* __restrict__ state,
+                                                          const int32_t* __restrict__ conn, int64_t N, int64_t E,
+                                                          const int32_t* __restrict__ eperm, HexCoef H,
+                                                          double* __restrict__ ek, double* __restrict__ er, long long* err) {
+  __shared__ double lanetab[32 * LANE_TAB];
+  __shared__ __align__(16) double scr[HXE_WARPS][HEX_SCRATCH];
+  __shared__ double stage[HXE_WARPS][36 * 9 + 24];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {  // per-lane constant table, as in the sweep kernel
+    const GeoFrag GF = geo_frag();
+    double* Lt = lanetab + tid;
+#pragma unroll
+    for (int s2 = 0; s2 < 2; s2++)
+#pragma unroll
+      for (int t = 0; t < 3; t++) Lt[32 * (s2 * 3 + t)] = GF.b[s2][t];
+    double g0[3], g1[3], N0, N1;
+    hex_ref(tid >> 2, tid & 3, g0, N0);
+    hex_ref(tid >> 2, (tid & 3) + 4, g1, N1);
+    for (int i = 0; i < 3; i++) { Lt[32 * (6 + i)] = g0[i]; Lt[32 * (9 + i)] = g1[i]; }
+    double gc[3], gc4[3], Nc, Nc4;
+    hex_ref(tid & 3, tid >> 2, gc, Nc);
+    hex_ref((tid & 3) + 4, tid >> 2, gc4, Nc4);
+    for (int i = 0; i < 3; i++) { Lt[32 * (12 + i)] = gc[i]; Lt[32 * (15 + i)] = gc4[i]; }
+  }
+  __syncthreads();
+  const int c = lane & 3, r = lane >> 2, q = r, a = r;
+  const double* L = lanetab + lane;
+  double* sc = scr[warp];
+  double* stg = stage[warp];
+  constexpr int RS = 22;
+  const int64_t nw = (int64_t)gridDim.x * HXE_WARPS;
+  for (int64_t pos = (int64_t)blockIdx.x * HXE_WARPS + warp; pos < E; pos += nw) {
+    const int64_t e = __ldg(eperm + pos);
+    const int nd = lane < 8 ? __ldg(conn + (int64_t)lane * E + e) : 0;
+    double av[2];
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+      const int node = __shfl_sync(0xffffffffu, nd, 4 * s + c);
+      av[s] = r < 3 ? __ldg(coords + (int64_t)r * N + node)
+                    : (HAS_R && r < 6) ? __ldg(state + (int64_t)(r - 3) * N + node) : 0.0;
+    }
+    double C3[3][2];
+#pragma unroll
+    for (int t = 0; t < 3; t++) { C3[t][0] = 0.0; C3[t][1] = 0.0; }
+#pragma unroll
+    for (int s = 0; s < 2; s++)
+#pragma unroll
+      for (int t = 0; t < 3; t++) dmma884(C3[t], av[s], L[32 * (s * 3 + t)]);
+    if (r < 6) {
+#pragma unroll
+      for (int t = 0; t < 3; t++) {
+        sc[hx_goff(r) + 8 * t + 2 * c] = C3[t][0];
+        sc[hx_goff(r) + 8 * t + 2 * c + 1] = C3[t][1];
+      }
+    }
+    __syncwarp();
+    double J[3][3], Dr[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        J[i][j] = sc[hx_goff(i) + 3 * q + j];
+        Dr[i][j] = HAS_R ? sc[hx_goff(3 + i) + 3 * q + j] : 0.0;
+      }
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    if (__any_sync(0xffffffffu, !(det > 0.0))) {
+      if (lane == 0) atomicCAS((unsigned long long*)err, (unsigned long long)(-1LL), (unsigned long long)e);
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();  // the GEMM output is consumed; the scratch takes the per-point records
+    const double rr = 1.0 / det;
+    double Ji[3][3];
+    Ji[0][0] = c00 * rr; Ji[1][0] = c01 * rr; Ji[2][0] = c02 * rr;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * rr;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * rr;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * rr;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * rr;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * rr;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * rr;
+    if (c == 0) {
+      double* o = sc + q * RS;
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int i = 0; i < 3; i++) o[j * 3 + i] = Ji[j][i];
+      o[9] = det;  // w (unit Gauss-Legendre weights)
+      if constexpr (HAS_R) {  // w σ_ij at the point
+        double gu[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; k++)
+#pragma unroll
+          for (int i = 0; i < 3; i++) gu[k][i] = Dr[k][0] * Ji[0][i] + Dr[k][1] * Ji[1][i] + Dr[k][2] * Ji[2][i];
+        const double lw = H.sl * det * (gu[0][0] + gu[1][1] + gu[2][2]), mw = H.sm * det;
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+          for (int j = 0; j < 3; j++) o[10 + i * 3 + j] = (i == j ? lw : 0.0) + mw * (gu[i][j] + gu[j][i]);
+      }
+    }
+    __syncwarp();
+    const double* o0 = sc + c * RS;
+    const double* o1 = sc + (c + 4) * RS;
+    double G0[3], G1[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      G0[i] = o0[0 * 3 + i] * L[32 * 6] + o0[1 * 3 + i] * L[32 * 7] + o0[2 * 3 + i] * L[32 * 8];
+      G1[i] = o1[0 * 3 + i] * L[32 * 9] + o1[1 * 3 + i] * L[32 * 10] + o1[2 * 3 + i] * L[32 * 11];
+    }
+    const double w0 = o0[9], w1 = o1[9];
+    if constexpr (HAS_R) {  // r_(a,i) = -Σ_γ Σ_j G_aj [w σ_ij]: lane (a, c < 2) gets rows (a, 2c), (a, 2c + 1)
+      double r2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        dmma884(r2, G0[j], r < 3 ? o0[10 + r * 3 + j] : 0.0);
+        dmma884(r2, G1[j], r < 3 ? o1[10 + r * 3 + j] : 0.0);
+      }
+      if (c == 0) { stg[324 + a * 3 + 0] = -r2[0]; stg[324 + a * 3 + 1] = -r2[1]; }
+      if (c == 1) stg[324 + a * 3 + 2] = -r2[0];
+    }
+    if constexpr (HAS_V) {  // Gram (18 DMMA) and K for columns b = 2c + t; upper blocks b >= a staged
+      double M[3][3][2];
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          M[j][k][0] = 0.0;
+          M[j][k][1] = 0.0;
+          dmma884(M[j][k], w0 * G0[j], G0[k]);
+          dmma884(M[j][k], w1 * G1[j], G1[k]);
+        }
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const int b = 2 * c + t;
+        if (b >= a) {
+          const double tr = M[0][0][t] + M[1][1][t] + M[2][2][t];
+          double* dst = stg + (a * 8 - a * (a - 1) / 2 + (b - a)) * 9;
+#pragma unroll
+          for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int m = 0; m < 3; m++) dst[i * 3 + m] = -(H.cl * M[i][m][t] + H.cm * M[m][i][t] + (i == m ? H.cm * tr : 0.0));
+        }
+      }
+    }
+    __syncwarp();
+    if constexpr (HAS_V) {
+      double* dst = ek + pos * 324;
+      for (int k = lane; k < 324; k += 32) dst[k] = stg[k];
+    }
+    if constexpr (HAS_R) {
+      if (lane < 24) er[pos * 24 + lane] = stg[324 + lane];
+    }
+    __syncwarp();  // scratch and stage are rewritten by the next element
+  }
+}
+
+// Q1 hexes, 2x2x2 points, every domain term ELAST_DOMAIN: the stored-mode element pass (all domain terms).
+int launch_hex_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
+                  double* ek, double* er, cudaStream_t s, bool* handled) {
+  *handled = false;
+  if (m->etype != ET_HEX || m->order != 1 || m->kh != 3 || m->physics != FEM_ELASTICITY || prob->quad_order != 2)
+    return 0;
+  HexCoef H = {0, 0, 0, 0, 0, 0};
+  int n_dom = 0;
+  for (int t = 0; t < prob->n_terms; t++) {
+    const fem_term& T = prob->terms[t];
+    if (T.region >= 0) continue;
+    if (T.form != FEM_WF_ELAST_DOMAIN) return 0;
+    const FormArgs F = make_form_args(prob, T);
+    H.cl += F.f0 * F.lam; H.cm += F.f0 * F.mu; H.sl += F.lam; H.sm += F.mu;
+    n_dom++;
+  }
+  if (!n_dom) return 0;
+  *handled = true;
+  if (m->E == 0) return 0;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto go = [&](auto kern) -> int {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * HXE_WARPS, 0);
+    const int64_t grid = std::min<int64_t>((m->E + HXE_WARPS - 1) / HXE_WARPS, (int64_t)sms * std::max(per_sm, 1));
+    kern<<<(unsigned)grid, 32 * HXE_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, m->E, eperm, H, ek, er, m->err);
+    FEM_CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  if (ek && er) return go(k_hex_el<true, true>);
+  if (ek) return go(k_hex_el<true, false>);
+  return go(k_hex_el<false, true>);
 }
 
 }  // namespace fem

@@ -6,8 +6,8 @@
 //   element  every element computes its whole local block K^e_(a,κ),(b,λ) (symmetric physics: the blocks
 //            a <= b) and residual d^e_(a,κ) and stores them at its position in the Morton order of element
 //            centroids — no conflicts, each element owns its storage (P2-tet elasticity: k_p2_el on the
-//            tensor cores, tet2_el.cu; P1-tet NS: k_ns_el, tet1_ns.cu; everything else: the generic element
-//            kernel); boundary terms add
+//            tensor cores, tet2_el.cu; Q1-hex elasticity: k_hex_el, hex_tiled.cu; P1-tet NS: k_ns_el,
+//            tet1_ns.cu; everything else: the generic element kernel); boundary terms add
 //            into the owning element's storage;
 //   gather   every scalar CSR slot s = (row point, column point) sums the blocks of the elements that
 //            contain both points, in a fixed list order (built once by a stable radix sort of the slot map),
@@ -125,6 +125,9 @@ void stored_free(fem_pattern_s* p) {
 // other domain forms or another quadrature order
 int launch_p2_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
                  double* ek, double* er, cudaStream_t s, bool* handled);
+// Q1-hex elasticity element pass (hex_tiled.cu), same contract
+int launch_hex_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
+                  double* ek, double* er, cudaStream_t s, bool* handled);
 // P1-tet NS (SUPG/PSPG) element pass (tet1_ns.cu), same contract
 int launch_ns_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
                  double* ek, double* er, cudaStream_t s, bool* handled);
@@ -352,6 +355,7 @@ int launch_stored(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem
     bool handled = false;
     rc = launch_p2_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
     if (!rc && !handled) rc = launch_ns_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
+    if (!rc && !handled) rc = launch_hex_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
     if (rc) return rc;
     if (handled) first = false;
   }

@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(TILED_THREADS, 1) k_ns_rec(const __grid_consta
       cp_async_commit();
     }
     const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
-    const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3], acc_n = P.values ? hdr[4] : 0;
+    const int T = hdr[0], H = hdr[1], nv = hdr[2], acc_n = P.values ? hdr[4] : 0;
     const uint32_t fmask = (uint32_t)hdr[5];
     const RecLayout L = rec_layout_hdr(NL, hdr);
     TileSmem D = S;

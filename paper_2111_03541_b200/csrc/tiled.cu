@@ -562,7 +562,7 @@ int tiles_build(fem_mesh_s* m, fem_pattern_s* p, cudaStream_t s) {
 template <int NL, int DIM>
 __device__ __forceinline__ void gather_halo_gen(const TiledParams& P, const uint8_t* rec, double* hbuf) {
   const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
-  const int T = hdr[0], H = hdr[1], nv = hdr[2], nr = hdr[3];
+  const int H = hdr[1];
   const RecLayout L = rec_layout_hdr(NL, hdr);
   const int32_t* hn = reinterpret_cast<const int32_t*>(rec + L.o_hnode);
   for (int t = threadIdx.x; t < H * P.hcomp; t += blockDim.x) {
