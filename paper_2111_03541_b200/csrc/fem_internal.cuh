@@ -196,6 +196,8 @@ struct fem_pattern_s {
   double* st_er = nullptr;     // [E][NL][KH]
   int64_t st_n_ent = 0;
   int st_nb = 0;               // blocks stored per element: NL(NL+1)/2 (symmetric physics, a <= b) or NL²
+  double* st_xaos = nullptr;   // P1-tet NS: node-major coordinates / state (32 bytes per point) for k_ns_el
+  double* st_saos = nullptr;
 };
 
 namespace fem {

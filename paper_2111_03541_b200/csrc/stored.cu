@@ -112,11 +112,12 @@ __global__ void __launch_bounds__(256) k_st_gather(const int64_t* __restrict__ r
 }
 
 void stored_free(fem_pattern_s* p) {
-  void* ptrs[] = {p->st_ent, p->st_off, p->st_rent, p->st_roff, p->st_epos, p->st_eperm, p->st_rows, p->st_ek, p->st_er};
+  void* ptrs[] = {p->st_ent, p->st_off, p->st_rent, p->st_roff, p->st_epos, p->st_eperm, p->st_rows, p->st_ek, p->st_er,
+                  p->st_xaos, p->st_saos};
   for (void* q : ptrs) cudaFree(q);
   p->st_ent = p->st_off = p->st_rent = p->st_roff = nullptr;
   p->st_epos = p->st_eperm = p->st_rows = nullptr;
-  p->st_ek = p->st_er = nullptr;
+  p->st_ek = p->st_er = p->st_xaos = p->st_saos = nullptr;
   p->st_n_ent = 0;
   p->st_nb = 0;
 }
@@ -130,7 +131,7 @@ int launch_hex_el(const fem_mesh_s* m, const fem_problem* prob, const double* st
                   double* ek, double* er, cudaStream_t s, bool* handled);
 // P1-tet NS (SUPG/PSPG) element pass (tet1_ns.cu), same contract
 int launch_ns_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
-                 double* ek, double* er, cudaStream_t s, bool* handled);
+                 double* ek, double* er, double* xaos, double* saos, cudaStream_t s, bool* handled);
 
 // Morton code of quantised coordinates (about one point per cell)
 struct MortonQ {
@@ -289,6 +290,13 @@ int fem_pattern_stored_prepare(fem_pattern_t p, int with_matrix, void* stream) {
     if (upload(&p->st_rows, rows, s)) return fail(FEM_E_OOM, "out of device memory for the row order");
     FEM_CUDA_TRY(cudaStreamSynchronize(s));
   }
+  if (m->physics == FEM_NS && m->etype == FEM_TET && m->order == 1 && !p->st_xaos) {  // k_ns_el's node-major copies
+    if (cudaMalloc(&p->st_xaos, sizeof(double) * 4 * (size_t)std::max<int64_t>(m->N, 1)) ||
+        cudaMalloc(&p->st_saos, sizeof(double) * 4 * (size_t)std::max<int64_t>(m->N, 1))) {
+      set_error("fem_pattern_stored_prepare: out of device memory for the node-major copies");
+      return FEM_E_OOM;
+    }
+  }
   if (!p->st_er) {
     if (cudaMalloc(&p->st_er, sizeof(double) * (size_t)std::max<int64_t>(E * NL * KH, 1))) {
       p->st_er = nullptr;
@@ -354,7 +362,7 @@ int launch_stored(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem
   {
     bool handled = false;
     rc = launch_p2_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
-    if (!rc && !handled) rc = launch_ns_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
+    if (!rc && !handled) rc = launch_ns_el(m, prob, state, p->st_eperm, ek, er, p->st_xaos, p->st_saos, s, &handled);
     if (!rc && !handled) rc = launch_hex_el(m, prob, state, p->st_eperm, ek, er, s, &handled);
     if (rc) return rc;
     if (handled) first = false;

@@ -440,12 +440,28 @@ int launch_ns_tiled(TiledParams& P, const TileSchedule& T, bool det, cudaStream_
 
 
 // ---- FEM_SCATTER_STORED element pass (stored.cu): the visit arithmetic of ns_compute for one element per
-// half-warp, its points gathered straight from HBM into the half's scratch; lane (a, b) stores the 4x4 block
+// half-warp, its points gathered from node-major copies (coordinates x y z 0 and state u1 u2 u3 p, 32 bytes
+// per point: one 256-bit load each) into the half's scratch; lane (a, b) stores the 4x4 block
 // (a, b) — f0·K, 16 doubles, four 256-bit stores — at ek[pos][a·4 + b] (all 16 blocks: NS is not symmetric)
 // and the residual entry (a, κ0 = b) at er[pos][a][b]; the element's 16 lanes write 2 KB contiguously.
 constexpr int NSE_WARPS = 8;
+// dst[i][c] = src[c][i] for c < ncomp, dst[i][c] = 0 for ncomp <= c < 4 (component-major -> node-major, 32 B/node)
+__global__ void k_aos4(const double* __restrict__ src, double* __restrict__ dst, int64_t n, int ncomp) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t >> 2;
+    const int c = (int)(t & 3);
+    dst[t] = c < ncomp ? __ldg(src + (int64_t)c * n + i) : 0.0;
+  }
+}
+static int aos4(const double* src, double* dst, int64_t n, int ncomp, cudaStream_t s) {
+  if (n <= 0) return 0;
+  const int64_t blocks = std::min<int64_t>((4 * n + 255) / 256, 148 * 64);
+  k_aos4<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n, ncomp);
+  FEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
 template <bool HAS_V, bool HAS_R>
-__global__ void __launch_bounds__(32 * NSE_WARPS) k_ns_el(const double* __restrict__ coords, const double* __restrict__ state,
+__global__ void __launch_bounds__(32 * NSE_WARPS) k_ns_el(const double* __restrict__ xaos, const double* __restrict__ saos,
                                                          const int32_t* __restrict__ conn, int64_t N, int64_t E,
                                                          const int32_t* __restrict__ eperm, NsCoef cf,
                                                          double* __restrict__ ek, double* __restrict__ er, long long* err) {
@@ -463,15 +479,20 @@ __global__ void __launch_bounds__(32 * NSE_WARPS) k_ns_el(const double* __restri
     const int64_t e = valid ? __ldg(eperm + pos) : 0;
     int node = 0;
     if (l16 < 4) node = valid ? __ldg(conn + (int64_t)l16 * E + e) : 0;
+    {  // the element's 4 points, node-major copies: lane (w, n) < 8 loads 32 bytes (x y z - or u1 u2 u3 p)
+      const int n = l16 & 3, wh = (l16 >> 2) & 1;
+      const int nn = __shfl_sync(0xffffffffu, node, (lane & 16) | n);
+      if (l16 < 8) {
+        double v[4];
+        if (valid) {
+          st_ld4((wh ? saos : xaos) + (int64_t)nn * 4, v[0], v[1], v[2], v[3]);
+        } else {  // (unit tet: det > 0)
 #pragma unroll
-    for (int k = 0; k < 2; k++) {  // 28 values over the 16 lanes: (component, node) = divmod(idx, 4)
-      const int idx = l16 + 16 * k;
-      const int src = (lane & 16) | (idx & 3);
-      const int nn = __shfl_sync(0xffffffffu, node, src);
-      if (idx < 28) {
-        const int comp = idx >> 2;
-        x[idx] = !valid ? (comp < 3 ? (double)((idx & 3) == comp + 1) : 0.0)  // (unit tet: det > 0)
-                        : comp < 3 ? __ldg(coords + (int64_t)comp * N + nn) : __ldg(state + (int64_t)(comp - 3) * N + nn);
+          for (int i = 0; i < 4; i++) v[i] = wh ? 0.0 : (double)(n == i + 1);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (wh || i < 3) x[(3 * wh + i) * 4 + n] = v[i];
       }
     }
     __syncwarp();
@@ -498,7 +519,7 @@ __global__ void __launch_bounds__(32 * NSE_WARPS) k_ns_el(const double* __restri
 
 // NS on P1 tets, 4-point rule, exactly one domain term NS_DOMAIN: the stored-mode element pass.
 int launch_ns_el(const fem_mesh_s* m, const fem_problem* prob, const double* state, const int32_t* eperm,
-                 double* ek, double* er, cudaStream_t s, bool* handled) {
+                 double* ek, double* er, double* xaos, double* saos, cudaStream_t s, bool* handled) {
   *handled = false;
   if (m->etype != ET_TET || m->order != 1 || m->kh != 4 || m->physics != FEM_NS || prob->quad_order != 2) return 0;
   int n_dom = 0, t_dom = -1;
@@ -507,6 +528,12 @@ int launch_ns_el(const fem_mesh_s* m, const fem_problem* prob, const double* sta
   if (n_dom != 1 || prob->terms[t_dom].form != FEM_WF_NS_DOMAIN) return 0;
   *handled = true;
   if (m->E == 0) return 0;
+  {  // node-major copies: coordinates once (padded to 4), the state per call
+    const int rc = aos4(m->coords, xaos, m->N, 3, s);
+    if (rc) return rc;
+    const int rc2 = aos4(state, saos, m->N, 4, s);
+    if (rc2) return rc2;
+  }
   const FormArgs F = make_form_args(prob, prob->terms[t_dom]);
   NsCoef cf;
   cf.rho = F.p[0]; cf.mu = F.p[1]; cf.tm = F.p[2]; cf.tc = F.p[3]; cf.f0 = F.f0;
@@ -516,7 +543,7 @@ int launch_ns_el(const fem_mesh_s* m, const fem_problem* prob, const double* sta
   auto go = [&](auto kern) -> int {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NSE_WARPS, 0);
     const int64_t grid = std::min<int64_t>((m->E + 2 * NSE_WARPS - 1) / (2 * NSE_WARPS), (int64_t)sms * std::max(per_sm, 1));
-    kern<<<(unsigned)grid, 32 * NSE_WARPS, 0, s>>>(m->coords, state, m->conn, m->N, m->E, eperm, cf, ek, er, m->err);
+    kern<<<(unsigned)grid, 32 * NSE_WARPS, 0, s>>>(xaos, saos, m->conn, m->N, m->E, eperm, cf, ek, er, m->err);
     FEM_CUDA_TRY(cudaGetLastError());
     return 0;
   };
