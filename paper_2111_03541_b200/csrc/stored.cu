@@ -103,11 +103,15 @@ __global__ void __launch_bounds__(256) k_st_gather(const int64_t* __restrict__ r
                                                    double* __restrict__ values, const uint32_t* __restrict__ roff,
                                                    const uint32_t* __restrict__ rent, const double* __restrict__ er,
                                                    double* __restrict__ rhs) {
+  // κ̂ = 4 (P1-tet NS rows: ≤ 15 slots): two rows per warp, 16 lanes each
+  constexpr int W = KH == 4 ? 16 : 32, RPW = 32 / W;
+  const int sub = (threadIdx.x & 31) / W;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_own; w += nw) {
-    const int64_t li = __ldg(rows + w);
-    if (values) st_gather_row<KH>(li, rowptr_s, nnz_s, off, ent, ek, values);
-    if (rhs) st_res_row<KH>(li, n_own, roff, rent, er, rhs);
+  for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW; w0 < n_own; w0 += nw * RPW) {
+    const int64_t w = w0 + sub;
+    const int64_t li = w < n_own ? (int64_t)__ldg(rows + w) : -1;
+    if (values && li >= 0) st_gather_row<KH, W>(li, rowptr_s, nnz_s, off, ent, ek, values);
+    if (rhs) st_res_row<KH, W>(li, n_own, roff, rent, er, rhs);
   }
 }
 

@@ -15,15 +15,15 @@ __device__ __forceinline__ void st_ld4(const double* p, double& a, double& b, do
   asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
-// One owned row li: lane per CSR slot of the row, the slot's stored blocks summed in list order (GU per
-// trip, all loads first), κ̂² values written.
-template <int KH>
+// One owned row li per W lanes (W = 32, or 16 for short rows: two rows per warp): lane per CSR slot of the
+// row, the slot's stored blocks summed in list order (GU per trip, all loads first), κ̂² values written.
+template <int KH, int W = 32>
 __device__ __forceinline__ void st_gather_row(int64_t li, const int64_t* __restrict__ rowptr_s, int64_t nnz_s,
                                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ ent,
                                               const double* ek, double* __restrict__ values) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   const int64_t rps = rowptr_s[li], deg = rowptr_s[li + 1] - rps;
-  for (int64_t o = lane; o < deg; o += 32) {
+  for (int64_t o = lane; o < deg; o += W) {
     const int64_t s = rps + o;
     double acc[KH * KH];
 #pragma unroll
@@ -65,26 +65,29 @@ __device__ __forceinline__ void st_gather_row(int64_t li, const int64_t* __restr
   }
 }
 
-// Residual row li: lane j takes entries j, j + 32, ... of the row's (pos·NL + a) list; the κ̂ components are
-// then reduced over the lanes by a fixed butterfly (deterministic) and lane 0 writes them.
-template <int KH>
+// Residual row li (W lanes per row; li < 0: no row, the lanes still take part in the shuffles): lane j
+// takes entries j, j + W, ... of the row's (pos·NL + a) list; the κ̂ components are then reduced over the
+// row's lanes by a fixed butterfly (deterministic) and its first lane writes them.  Called by all 32 lanes.
+template <int KH, int W = 32>
 __device__ __forceinline__ void st_res_row(int64_t li, int64_t n_own, const uint32_t* __restrict__ roff,
                                            const uint32_t* __restrict__ rent, const double* er, double* __restrict__ rhs) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   double acc[KH];
 #pragma unroll
   for (int k = 0; k < KH; k++) acc[k] = 0.0;
-  const uint32_t j1 = __ldg(roff + li + 1);
-  for (uint32_t j = __ldg(roff + li) + lane; j < j1; j += 32) {
-    const double* src = er + (int64_t)__ldg(rent + j) * KH;
+  if (li >= 0) {
+    const uint32_t j1 = __ldg(roff + li + 1);
+    for (uint32_t j = __ldg(roff + li) + lane; j < j1; j += W) {
+      const double* src = er + (int64_t)__ldg(rent + j) * KH;
 #pragma unroll
-    for (int k = 0; k < KH; k++) acc[k] += __ldg(src + k);
+      for (int k = 0; k < KH; k++) acc[k] += __ldg(src + k);
+    }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1)
+  for (int o = W / 2; o; o >>= 1)
 #pragma unroll
     for (int k = 0; k < KH; k++) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-  if (lane == 0) {
+  if (lane == 0 && li >= 0) {
 #pragma unroll
     for (int k = 0; k < KH; k++) rhs[(int64_t)k * n_own + li] = acc[k];
   }
