@@ -103,8 +103,9 @@ __global__ void __launch_bounds__(256) k_st_gather(const int64_t* __restrict__ r
                                                    double* __restrict__ values, const uint32_t* __restrict__ roff,
                                                    const uint32_t* __restrict__ rent, const double* __restrict__ er,
                                                    double* __restrict__ rhs) {
-  // κ̂ = 4 (P1-tet NS rows: ≤ 15 slots): two rows per warp, 16 lanes each
-  constexpr int W = KH == 4 ? 16 : 32, RPW = 32 / W;
+  // κ̂ = 4 (P1-tet NS rows: ≤ 15 slots): four rows per warp, 8 lanes each (c4: 32 lanes 33.0, 16 lanes
+  // 27.2, 8 lanes 25.6, 4 lanes 27.2 ms); κ̂ = 3 keeps a warp per row (c3: 8 lanes 5.2 vs 4.9 ms)
+  constexpr int W = KH == 4 ? 8 : 32, RPW = 32 / W;
   const int sub = (threadIdx.x & 31) / W;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW; w0 < n_own; w0 += nw * RPW) {
