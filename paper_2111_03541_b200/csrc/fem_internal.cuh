@@ -196,6 +196,9 @@ struct fem_pattern_s {
   double* st_er = nullptr;     // [E][NL][KH]
   int64_t st_n_ent = 0;
   int st_nb = 0;               // blocks stored per element: NL(NL+1)/2 (symmetric physics, a <= b) or NL²
+  // boundary sets re-grouped for the stored mode: facets only conflict when they belong to the same element
+  // (each element owns its storage), so group g of a set holds each element's g-th facet (≤ 6 groups)
+  std::vector<fem::TaskList> st_bnd;
   double* st_xaos = nullptr;   // P1-tet NS: node-major coordinates / state (32 bytes per point) for k_ns_el
   double* st_saos = nullptr;
 };

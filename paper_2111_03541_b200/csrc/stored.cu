@@ -125,6 +125,8 @@ void stored_free(fem_pattern_s* p) {
   p->st_ek = p->st_er = p->st_xaos = p->st_saos = nullptr;
   p->st_n_ent = 0;
   p->st_nb = 0;
+  for (auto& L : p->st_bnd) { cudaFree(L.elem); cudaFree(L.facet); }
+  p->st_bnd.clear();
 }
 
 // P2-tet elasticity element pass on the tensor cores (tet2_el.cu): *handled = false when the problem has
@@ -293,6 +295,31 @@ int fem_pattern_stored_prepare(fem_pattern_t p, int with_matrix, void* stream) {
     std::vector<int32_t> rows(n_own);
     for (int64_t i = 0; i < n_own; i++) rows[i] = rk[i].second;
     if (upload(&p->st_rows, rows, s)) return fail(FEM_E_OOM, "out of device memory for the row order");
+    // 4. boundary facets grouped by their rank within their element (stable: set order inside a group)
+    for (size_t k = 0; k < m->h_bset_elem.size(); k++) {
+      const auto& be = m->h_bset_elem[k];
+      const auto& bf = m->h_bset_facet[k];
+      std::vector<std::pair<int32_t, int32_t>> key(be.size());  // (rank, index)
+      std::vector<uint8_t> seen(E, 0);
+      for (size_t j = 0; j < be.size(); j++) key[j] = {seen[be[j]]++, (int32_t)j};
+      std::stable_sort(key.begin(), key.end());
+      std::vector<int32_t> el(be.size());
+      std::vector<int8_t> fa(be.size());
+      TaskList L;
+      L.n = (int64_t)be.size();
+      L.col_off.push_back(0);
+      for (size_t j = 0; j < key.size(); j++) {
+        el[j] = be[key[j].second];
+        fa[j] = bf[key[j].second];
+        if (j && key[j].first != key[j - 1].first) L.col_off.push_back((int64_t)j);
+      }
+      L.col_off.push_back(L.n);
+      if (upload(&L.elem, el, s) || upload(&L.facet, fa, s)) {
+        cudaFree(L.elem);
+        return fail(FEM_E_OOM, "out of device memory for the boundary groups");
+      }
+      p->st_bnd.push_back(L);
+    }
     FEM_CUDA_TRY(cudaStreamSynchronize(s));
   }
   if (m->physics == FEM_NS && m->etype == FEM_TET && m->order == 1 && !p->st_xaos) {  // k_ns_el's node-major copies
@@ -322,8 +349,9 @@ int fem_pattern_stored_prepare(fem_pattern_t p, int with_matrix, void* stream) {
 
 namespace fem {
 
-// Boundary terms into storage: one facet colour per launch (facets of one element have distinct colours:
-// they share its points), sets in term order, added (the storage holds the domain part, or zeros).
+// Boundary terms into storage: the facets of one element must not be added concurrently (they share its
+// storage; facets of different elements never conflict), so a set runs as ≤ 6 launches — group g holds each
+// element's g-th facet — in term order, added (the storage holds the domain part, or zeros).
 static int stored_facets(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem* prob, const double* state,
                          double* ek, double* er, const int32_t* map, cudaStream_t s) {
   for (int t = 0; t < prob->n_terms; t++) {
@@ -337,7 +365,7 @@ static int stored_facets(const fem_mesh_s* m, const fem_pattern_s* p, const fem_
     A.ek_add = 1;
     A.ek_map = map;
     if (!A.ek && !A.er) continue;
-    const TaskList& L = m->bnd[T.region];
+    const TaskList& L = p->st_bnd[T.region];
     A.task_elem = L.elem;
     A.task_facet = L.facet;
     for (size_t c = 0; c + 1 < L.col_off.size(); c++) {
