@@ -96,7 +96,7 @@ __global__ void k_st_rfill(const int64_t* __restrict__ diag, const uint32_t* __r
 }
 
 // ---- two-phase path, gather: warp per owned row in the gather order
-template <int KH>
+template <int KH, bool RES_ONLY>
 __global__ void __launch_bounds__(256) k_st_gather(const int64_t* __restrict__ rowptr_s, int64_t n_own, int64_t nnz_s,
                                                    const int32_t* __restrict__ rows, const uint32_t* __restrict__ off,
                                                    const uint32_t* __restrict__ ent, const double* __restrict__ ek,
@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(256) k_st_gather(const int64_t* __restrict__ r
                                                    double* __restrict__ rhs) {
   // κ̂ = 4 (P1-tet NS rows: ≤ 15 slots): four rows per warp, 8 lanes each (c4: 32 lanes 33.0, 16 lanes
   // 27.2, 8 lanes 25.6, 4 lanes 27.2 ms); κ̂ = 3 keeps a warp per row (c3: 8 lanes 5.2 vs 4.9 ms)
-  constexpr int W = KH == 4 ? 8 : 32, RPW = 32 / W;
+  // residual-only calls: a row has one entry per element (8-24), 8 lanes per row
+  constexpr int W = (KH == 4 || RES_ONLY) ? 8 : 32, RPW = 32 / W;
   const int sub = (threadIdx.x & 31) / W;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW; w0 < n_own; w0 += nw * RPW) {
@@ -427,8 +428,8 @@ int launch_stored(const fem_mesh_s* m, const fem_pattern_s* p, const fem_problem
   if (m->n_own) {
     const int grid = grid_of(m->n_own * 32);
 #define ST_GATHER(K)                                                                                             \
-  k_st_gather<K><<<grid, 256, 0, s>>>(p->rowptr_s, m->n_own, p->nnz_s, p->st_rows, p->st_off, p->st_ent, ek, values, \
-                                      p->st_roff, p->st_rent, er, rhs)
+  (values ? k_st_gather<K, false> : k_st_gather<K, true>)<<<grid, 256, 0, s>>>(                                  \
+      p->rowptr_s, m->n_own, p->nnz_s, p->st_rows, p->st_off, p->st_ent, ek, values, p->st_roff, p->st_rent, er, rhs)
     if (KH == 1) ST_GATHER(1);
     else if (KH == 2) ST_GATHER(2);
     else if (KH == 3) ST_GATHER(3);
