@@ -206,16 +206,23 @@ template <> struct Elem<ET_HEX, 1> {
 // Node a sits at ξ = q_a ∈ {-1,0,1}³: corners in VTK order, the 12 edge midpoints of VTK's quadratic
 // hexahedron, then (27-node) the face centres in facet order x-,x+,y-,y+,z-,z+ and the centre.
 // Encoded as base-3 digits (q+1) per axis, x fastest: corners 0,2,8,6,18,20,26,24 etc.
-__host__ __device__ inline int qc_code(int a) {
-  const int T[27] = {0, 2, 8, 6, 18, 20, 26, 24,                   // corners (---),(+--),(++-),(-+-),(--+)...
-                     1, 5, 7, 3, 19, 23, 25, 21, 9, 11, 17, 15,    // edges (0,1),(1,2),(2,3),(3,0),(4,5)...(3,7)
-                     12, 14, 10, 16, 4, 22, 13};                   // faces x-,x+,y-,y+,z-,z+; centre
-  return T[a];
+constexpr int kQcCode[27] = {0, 2, 8, 6, 18, 20, 26, 24,                 // corners (---),(+--),(++-),(-+-),(--+)...
+                             1, 5, 7, 3, 19, 23, 25, 21, 9, 11, 17, 15,  // edges (0,1),(1,2),(2,3),(3,0),(4,5)...(3,7)
+                             12, 14, 10, 16, 4, 22, 13};                 // faces x-,x+,y-,y+,z-,z+; centre
+// the digits (q+1 per axis, 2 bits each) of nodes 10w .. 10w+9 packed into one word at compile time, so a
+// lookup is a shift and a mask (no per-call local array)
+constexpr uint64_t qc_pack(int w) {
+  uint64_t r = 0;
+  for (int i = 0; i < 10 && 10 * w + i < 27; i++) {
+    const int c = kQcCode[10 * w + i];
+    r |= (uint64_t)((c % 3) | ((c / 3) % 3) << 2 | (c / 9) << 4) << (6 * i);
+  }
+  return r;
 }
 __host__ __device__ inline int qc_coord(int a, int d) {  // q_a,d ∈ {-1,0,1}
-  int c = qc_code(a);
-  for (int k = 0; k < d; k++) c /= 3;
-  return c % 3 - 1;
+  constexpr uint64_t W0 = qc_pack(0), W1 = qc_pack(1), W2 = qc_pack(2);
+  const uint64_t w = a < 10 ? W0 : a < 20 ? W1 : W2;
+  return (int)((w >> (6 * (a % 10) + 2 * d)) & 3u) - 1;
 }
 // 1D quadratic Lagrange basis on {-1,0,1}: (value, first, second derivative) of node q at t
 __host__ __device__ inline void lq1(int q, double t, double& v, double& d1, double& d2) {

@@ -50,9 +50,10 @@ struct Q2Cfg {
   static constexpr int RP = (R + 7) / 8 * 8;    // padded to the 8-row tiles
   static constexpr int NT = RP / 8;             // tiles per side
   static constexpr int MS = RP + 1;             // row stride of M in shared memory (odd: fewer conflicts)
-  // shared memory (doubles): X[3][NL] | D[3][NL] | Gm[RP][KP] | w[KP] | Ji[NQ][9] | Sw[NQ][9] | M[RP][MS]
+  // shared memory (doubles): X[3][NL] | D[3][NL] | Gm[RP][KP] | w[KP] | Ji[NQ][9] | Sw[NQ][9] | M[RP][MS] |
+  // ref[NQ][NL][3] (the reference gradients ∇̂N_a(ξ_γ), the same for every element: built once per CTA)
   static constexpr int O_X = 0, O_D = 3 * NL, O_G = 6 * NL, O_W = O_G + RP * KP, O_JI = O_W + KP,
-                       O_S = O_JI + 9 * NQ, O_M = O_S + 9 * NQ, TOTAL = O_M + RP * MS;
+                       O_S = O_JI + 9 * NQ, O_M = O_S + 9 * NQ, O_REF = O_M + RP * MS, TOTAL = O_REF + 3 * NQ * NL;
 };
 
 template <int ET, int Q1D, bool HAS_V, bool HAS_R>
@@ -67,9 +68,17 @@ __global__ void __launch_bounds__(Q2_THREADS) k_q2_elast(const GenParams P) {
   double* Ji = q2s + C::O_JI;
   double* Sw = q2s + C::O_S;
   double* M = q2s + C::O_M;
+  double* ref = q2s + C::O_REF;
   __shared__ int nodes[NL];
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int t = tid; t < NQ * NL; t += Q2_THREADS) {
+    const int q = t / NL, a = t % NL;
+    double xi[3], wr;
+    Elem<ET_HEX, 1>::vol_qp(Q1D, q, xi, wr);
+    q2_node_grad<ET>(a, xi, ref + 3 * t);
+  }
+  __syncthreads();
   const double lam = P.F.lam, mu = P.F.mu, f0 = P.F.f0;
   for (int64_t task = blockIdx.x; task < P.task_count; task += gridDim.x) {
     const int64_t ti = P.task_begin + task;
@@ -94,8 +103,7 @@ __global__ void __launch_bounds__(Q2_THREADS) k_q2_elast(const GenParams P) {
       Elem<ET_HEX, 1>::vol_qp(Q1D, tid, xi, wr);
       double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
       for (int a = 0; a < NL; a++) {
-        double g[3];
-        q2_node_grad<ET>(a, xi, g);
+        const double* g = ref + 3 * (tid * NL + a);
 #pragma unroll
         for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -116,10 +124,7 @@ __global__ void __launch_bounds__(Q2_THREADS) k_q2_elast(const GenParams P) {
     // ---- gradient table Gm[(a, j)][γ] = (J^{-T} ∇̂N_a(ξ_γ))_j
     for (int t = tid; t < NL * NQ; t += Q2_THREADS) {
       const int a = t / NQ, q = t % NQ;
-      double xi[3], wr;
-      Elem<ET_HEX, 1>::vol_qp(Q1D, q, xi, wr);
-      double g[3];
-      q2_node_grad<ET>(a, xi, g);
+      const double* g = ref + 3 * (q * NL + a);
       const double* J = Ji + q * 9;
 #pragma unroll
       for (int i = 0; i < 3; i++) Gm[(3 * a + i) * KP + q] = J[0 * 3 + i] * g[0] + J[1 * 3 + i] * g[1] + J[2 * 3 + i] * g[2];
