@@ -76,3 +76,29 @@ def test_stored_inverted_element_reported():
     rc, bad = S.status()
     assert rc == -4 and bad == 0
     S.close()
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_stored_through_the_host_entry_points(name):
+    """fem_linearize_host / _async (host state in, norms out) with FEM_SCATTER_STORED: the same matrix,
+    residual and norms as the device call, bit for bit, call after call."""
+    _need_gpu()
+    from paper_2111_03541_b200 import fem
+    m, p = make_config(name, "perturbed", {"c3": (7, 3, 2), "c4": (9, 4, 3)}[name])
+    st = make_state(name, m, p)
+    from paper_2111_03541_b200 import FemSystem
+    S = FemSystem(m, p)
+    v_dev, r_dev = [x.clone() for x in S.system(torch.from_numpy(st).cuda(), scatter="stored")]
+    n_dev = torch.zeros(2, dtype=torch.float64, device="cuda")
+    fem.fem_residual_norms(S.mesh_h, r_dev, n_dev)
+    hs = torch.from_numpy(st).pin_memory()
+    n_sync = torch.zeros(2, dtype=torch.float64).pin_memory()
+    fem.fem_linearize_host(S.mesh_h, S.pat_h, p, hs, S.values, S.rhs, n_sync, "stored", P=S.P)
+    assert torch.equal(S.values, v_dev) and torch.equal(S.rhs, r_dev)
+    assert torch.equal(n_sync, n_dev.cpu())
+    n_async = torch.zeros(2, dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        fem.fem_linearize_host_async(S.mesh_h, S.pat_h, p, hs, S.values, S.rhs, n_async, "stored", P=S.P)
+    torch.cuda.synchronize()
+    assert torch.equal(S.values, v_dev) and torch.equal(S.rhs, r_dev) and torch.equal(n_async, n_sync)
+    S.close()
