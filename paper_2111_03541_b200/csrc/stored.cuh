@@ -1,5 +1,5 @@
-// stored.cuh — device side of FEM_SCATTER_STORED (stored.cu): the per-slot gather of one owned row and
-// its residual row, shared by the gather kernel and the element kernels' launchers.
+// stored.cuh — device side of FEM_SCATTER_STORED (stored.cu): the per-slot gather of one owned row and its
+// residual row, and the 256-bit load/store helpers shared with the element passes (tet1_ns.cu).
 #pragma once
 #include <cstdint>
 
@@ -15,7 +15,7 @@ __device__ __forceinline__ void st_ld4(const double* p, double& a, double& b, do
   asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
-// One owned row li per W lanes (W = 32, or 16 for short rows: two rows per warp): lane per CSR slot of the
+// One owned row li per W lanes (W = 32, or 8 for short rows: four rows per warp): lane per CSR slot of the
 // row, the slot's stored blocks summed in list order (GU per trip, all loads first), κ̂² values written.
 template <int KH, int W = 32>
 __device__ __forceinline__ void st_gather_row(int64_t li, const int64_t* __restrict__ rowptr_s, int64_t nnz_s,

@@ -6,10 +6,10 @@
 // Rm_i(γ) = ρ u_k(γ) u_i,k + p_,i is linear in u(γ) (u_i,kk = 0, reading L10).  A warp takes two
 // element visits at once: lane (h, a, b) with h = lane>>4 computes the geometry of visit h and the
 // 4x4 block of the pair (a, b) summed over the 4 points; the same lanes then take the residual rows
-// (a, κ0).  Contributions go to the tile accumulator with shared-memory fp64 atomics (CAS loops on
-// sm_100), or, with FEM_NS_DET, with plain read-modify-writes in record order (per-row turns,
-// bit-identical run to run, ~25% slower on c4).  Boundary groups (inflow/outflow/fix) reuse the generic
-// warp path.
+// (a, κ0).  Contributions go to the tile accumulator with plain read-modify-writes in record order under
+// per-row turns (FEM_SCATTER_TILED: bit-identical run to run) or with shared-memory fp64 atomics
+// (FEM_SCATTER_TILED_UNORDERED).  Boundary groups (inflow/outflow/fix) run as the coloured generic facet
+// pass.  The element arithmetic (ns_compute) is shared with the stored-mode element pass k_ns_el.
 #include <algorithm>
 #include <cstdlib>
 #include <string>
